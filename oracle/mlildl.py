@@ -1,0 +1,344 @@
+"""Multilevel incomplete LDL^T preconditioner (TEST INFRASTRUCTURE ONLY -- see
+oracle/__init__.py).
+
+Follows PAPER.md sect. 7 (l.790-973) step by step, in the independent-set
+reading fixed in DESIGN.md sect. 3.3 (readings R6-R12).  Per level l, with the
+level matrix A_l (symmetric, explicit diagonal):
+
+ (i)  Reordering/scaling, sect. 7.1 (l.800-819): D_i = 1/sqrt(max_j |a_ij|),
+      A^ = D A D computed as a_ij * (D_i * D_j).
+ (ii) Pivot selection, sect. 7.2 (l.821-915):
+      - 1x1 quality: lmax1_f = max_{j!=f}|a^_jf| / |a^_ff|,
+        d1_f = sum_{j!=f}|a^_jf| / |a^_ff|                      (paper's d_1, l.866)
+      - 2x2 pivots from a symmetric matching, sect. 6.2 (l.623-677): every node
+        proposes its strongest neighbour p(i) = argmax_{j!=i}|a^_ij|; mutual
+        proposals {i, p(i)} in which at least one member fails the 1x1 bound
+        become 2x2 candidates B = [[a^_ii, a^_ij],[a^_ij, a^_jj]]; accepted iff
+        det B != 0, d2 < d1_lead (the paper's "2x2 update only if d2 < d1",
+        l.874) and lmax2 <= kappa-1.
+      - inverse-based bound (l.884-896): the new block column of L may not push
+        ||L^{-1}||_inf above kappa: each single column entry |l_cf| <= kappa-1
+        (candidate test) and every row sum of |L| <= kappa-1 (budget repair);
+        violators are postponed to the next level (l.895-897).
+      - level 0 on the lattice: the red sites of the bipartite split
+        (reading R6); levels > 0: a maximal independent set of candidate
+        blocks in the strong graph |a^_ij| >= tau_strong, lowest (quality,
+        leader) first, synchronous rounds (reading R9).
+ (iii) Factor: L = A^_CF B^{-1} (entries < tau_drop dropped, the paper's
+      "drop these entries whenever their absolute value is less than
+      eps/kappa", l.909-911), S = A^_CC - A^_CF B^{-1} A^_FC symmetrised and
+      off-diagonals < tau_drop dropped (reading R10), F-F couplings (all weak
+      by construction of the independent set) are dropped.
+ (iv) Recursion on S (sect. 7.3, l.917-945) until n <= n_coarse_max, the level
+      cap, or a level eliminates < stall_frac*n nodes; the last Schur
+      complement is inverted densely.
+Application (sect. 7.4 l.975-987 / reading R11): z = M^{-1} r with the block
+forward / backward substitution, L_21 applied from its stored (dropped) entries.
+"""
+import numpy as np
+import scipy.sparse as sp
+
+from .anderson import red_sites
+
+
+class Level:
+    pass
+
+
+def _scaled(A):
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    coo = A.tocoo()
+    r, c, v = coo.row, coo.col, coo.data
+    rowmax = np.zeros(n)
+    np.maximum.at(rowmax, r, np.abs(v))
+    D = np.where(rowmax > 0, 1.0 / np.sqrt(np.where(rowmax > 0, rowmax, 1.0)), 1.0)
+    ah = v * (D[r] * D[c])
+    Ah = sp.csr_matrix((ah, (r, c)), shape=(n, n))
+    Ah.sort_indices()
+    return D, Ah
+
+
+def _pivot_quality(Ah):
+    n = Ah.shape[0]
+    coo = Ah.tocoo()
+    r, c, v = coo.row, coo.col, coo.data
+    off = r != c
+    dg = Ah.diagonal()
+    cm = np.zeros(n)
+    np.maximum.at(cm, r[off], np.abs(v[off]))
+    osum = np.zeros(n)
+    np.add.at(osum, r[off], np.abs(v[off]))
+    adg = np.abs(dg)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lmax1 = np.where(adg > 0, cm / np.where(adg > 0, adg, 1.0), np.inf)
+        d1 = np.where(adg > 0, osum / np.where(adg > 0, adg, 1.0), np.inf)
+    # strongest neighbour proposal p(i) (ties -> smallest j)
+    p = np.full(n, -1, dtype=np.int64)
+    ro, co, vo = r[off], c[off], np.abs(v[off])
+    order = np.lexsort((co, -vo, ro))
+    ro, co = ro[order], co[order]
+    first = np.ones(len(ro), bool)
+    first[1:] = ro[1:] != ro[:-1]
+    p[ro[first]] = co[first]
+    return dg, lmax1, d1, p
+
+
+def _pair_candidates(Ah, dg, lmax1, d1, p, kappa):
+    """2x2 pivots from mutual strongest-neighbour proposals (sect. 6.2 / 7.2)."""
+    n = Ah.shape[0]
+    ok1 = (lmax1 <= kappa - 1) & (dg != 0)
+    pairs = []
+    idx = np.arange(n)
+    has = p >= 0
+    mutual = has.copy()
+    mutual[has] = p[p[has]] == idx[has]
+    cand = np.where(mutual & (idx < p) & ~(ok1 & ok1[np.maximum(p, 0)]))[0]
+    for i in cand:
+        j = int(p[i])
+        aii, ajj, aij = dg[i], dg[j], Ah[i, j]
+        det = aii * ajj - aij * aij
+        if det == 0.0:
+            continue
+        B11, B12, B22 = ajj / det, -aij / det, aii / det
+        ri = Ah.getrow(i).tocoo()
+        rj = Ah.getrow(j).tocoo()
+        ai = dict(zip(ri.col.tolist(), ri.data.tolist()))
+        aj = dict(zip(rj.col.tolist(), rj.data.tolist()))
+        nbrs = (set(ai) | set(aj)) - {i, j}
+        lm2, d2 = 0.0, 0.0
+        for cc in nbrs:
+            aci, acj = ai.get(cc, 0.0), aj.get(cc, 0.0)
+            w = abs(aci * B11 + acj * B12) + abs(aci * B12 + acj * B22)
+            lm2 = max(lm2, w)
+            d2 += w
+        lead = i if not ok1[i] else j
+        if d2 < d1[lead] and lm2 <= kappa - 1:
+            pairs.append((i, j, B11, B12, B22, lm2))
+    return pairs
+
+
+def _mis(nb, keyrank, edges_a, edges_b):
+    """Synchronous maximal independent set on blocks (reading R9): a block
+    wins when its rank is below every undecided neighbour's rank."""
+    und = np.ones(nb, bool)
+    sel = np.zeros(nb, bool)
+    rounds = 0
+    while und.any():
+        rounds += 1
+        ru = np.where(und, keyrank, np.iinfo(np.int64).max)
+        nbmin = np.full(nb, np.iinfo(np.int64).max)
+        np.minimum.at(nbmin, edges_a, ru[edges_b])
+        win = und & (keyrank < nbmin)
+        sel |= win
+        hit = np.zeros(nb, bool)
+        hit[edges_a[win[edges_b]]] = True
+        und &= ~win & ~hit
+    return sel, rounds
+
+
+def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.005):
+    n = A.shape[0]
+    D, Ah = _scaled(A)
+    dg, lmax1, d1, p = _pivot_quality(Ah)
+    ok1 = (lmax1 <= kappa - 1) & (dg != 0)
+
+    # ---- blocks: accepted 2x2 pairs and 1x1 singles -------------------------
+    partner = np.full(n, -1, dtype=np.int64)
+    b11 = np.zeros(n)
+    b12 = np.zeros(n)
+    if lattice_L is None:
+        pairs = _pair_candidates(Ah, dg, lmax1, d1, p, kappa)
+    else:
+        pairs = []
+    leader = np.full(n, -1, dtype=np.int64)     # block leader of each candidate node
+    q = np.full(n, np.inf)                      # block quality (at the leader)
+    for (i, j, B11, B12, B22, lm2) in pairs:
+        partner[i], partner[j] = j, i
+        b11[i], b12[i] = B11, B12
+        b11[j], b12[j] = B22, B12
+        leader[i] = leader[j] = i
+        q[i] = lm2
+    singles = ok1 & (partner < 0)
+    leader[singles] = np.where(singles)[0]
+    q[singles] = lmax1[singles]
+    with np.errstate(divide="ignore"):
+        b11[singles] = 1.0 / dg[singles]
+
+    # ---- independent set ------------------------------------------------------
+    if lattice_L is not None:
+        inF = singles & red_sites(lattice_L)
+        rounds = 0
+    else:
+        blk = np.where(leader == np.arange(n))[0]           # block ids = leaders
+        nb = len(blk)
+        bid = np.full(n, -1, dtype=np.int64)
+        pos = np.full(n, -1, dtype=np.int64)
+        pos[blk] = np.arange(nb)
+        m = leader >= 0
+        bid[m] = pos[leader[m]]
+        keyrank = np.empty(nb, dtype=np.int64)
+        keyrank[np.lexsort((blk, q[blk]))] = np.arange(nb)
+        coo = Ah.tocoo()
+        r, c, v = coo.row, coo.col, coo.data
+        strong = (r != c) & (np.abs(v) >= tau_strong) & (bid[r] >= 0) & (bid[c] >= 0)
+        ea, eb = bid[r[strong]], bid[c[strong]]
+        keep = ea != eb
+        sel, rounds = _mis(nb, keyrank, ea[keep], eb[keep])
+        inF = np.zeros(n, bool)
+        inF[m] = sel[bid[m]]
+
+    # ---- row-budget repair: rows of L^{-1} bounded by kappa (l.884-897) -------
+    coo = Ah.tocoo()
+    r, c, v = coo.row, coo.col, coo.data
+    off = r != c
+    r, c, v = r[off], c[off], v[off]
+    repair_rounds = 0
+    while True:
+        Lfull = _lfull(Ah, inF, partner, b11, b12, dg)
+        Lc = Lfull.tocoo()
+        rows_c = Lc.row                     # these are level indices of C nodes
+        lead_of = np.where(partner[Lc.col] >= 0, np.minimum(Lc.col, partner[Lc.col]), Lc.col)
+        w = np.abs(Lc.data)
+        # aggregate per (c, block)
+        key = rows_c * n + lead_of
+        uk, inv = np.unique(key, return_inverse=True)
+        wb = np.zeros(len(uk))
+        np.add.at(wb, inv, w)
+        bc, bl = uk // n, uk % n
+        budget = np.zeros(n)
+        np.add.at(budget, bc, wb)
+        viol = budget > kappa - 1
+        if not viol.any():
+            break
+        repair_rounds += 1
+        # nominate the largest contributor per violating row (ties -> smallest leader)
+        mv = viol[bc]
+        o = np.lexsort((bl[mv], -wb[mv], bc[mv]))
+        cc, ll = bc[mv][o], bl[mv][o]
+        firstc = np.ones(len(cc), bool)
+        firstc[1:] = cc[1:] != cc[:-1]
+        rm = ll[firstc]
+        inF[rm] = False
+        pr = partner[rm]
+        inF[pr[pr >= 0]] = False
+
+    nF = int(inF.sum())
+    if nF < stall_frac * n:
+        return None
+
+    # ---- factor ------------------------------------------------------------------
+    Lv = Level()
+    Lv.n = n
+    Lv.D = D
+    Lv.inF = inF
+    Lv.F = np.where(inF)[0]
+    Lv.C = np.where(~inF)[0]
+    Lv.partner = np.where(inF, partner, -1)
+    Lv.b11 = np.where(inF, b11, 0.0)
+    Lv.b12 = np.where(inF & (partner >= 0), b12, 0.0)
+    Lv.npairs = int(((partner >= 0) & inF).sum() // 2)
+    Lv.rounds = rounds
+    Lv.repair_rounds = repair_rounds
+    Lfull = _lfull(Ah, inF, partner, b11, b12, dg)          # rows: level idx (C only)
+    Lc = Lfull.tocoo()
+    keep = np.abs(Lc.data) >= tau_drop
+    cmap = np.full(n, -1, dtype=np.int64)
+    cmap[Lv.C] = np.arange(len(Lv.C))
+    Lv.cmap = cmap
+    # L stored with rows = coarse index, cols = level index (F nodes)
+    Lv.L = sp.csr_matrix((Lc.data[keep], (cmap[Lc.row[keep]], Lc.col[keep])), shape=(len(Lv.C), n))
+    Lv.L.sort_indices()
+    Binv = _binv(n, inF, partner, b11, b12)
+    AhCF = Ah[Lv.C][:, Lv.F]
+    S = Ah[Lv.C][:, Lv.C] - AhCF @ Binv[Lv.F][:, Lv.F] @ AhCF.T
+    S = sp.csr_matrix(S)
+    S = 0.5 * (S + S.T)                           # exact symmetry (reading R10)
+    S = S.tocoo()
+    keepS = (S.row == S.col) | (np.abs(S.data) >= tau_drop)
+    nC = len(Lv.C)
+    S = sp.csr_matrix((S.data[keepS], (S.row[keepS], S.col[keepS])), shape=(nC, nC))
+    # explicit diagonal even when zero
+    dS = S.diagonal()
+    S = S + sp.csr_matrix((np.zeros(nC), (np.arange(nC), np.arange(nC))), shape=(nC, nC))
+    S = sp.csr_matrix(S)
+    S.sort_indices()
+    assert np.array_equal(S.diagonal(), dS)
+    Lv.S = S
+    Lv.Binv = Binv
+    return Lv
+
+
+def _binv(n, inF, partner, b11, b12):
+    """Block-diagonal B^{-1} on F nodes (1x1: 1/a^_ff; 2x2: inverse of the pair)."""
+    f = np.where(inF)[0]
+    rows = [f]
+    cols = [f]
+    vals = [b11[f]]
+    pf = f[partner[f] >= 0]
+    rows.append(pf)
+    cols.append(partner[pf])
+    vals.append(b12[pf])
+    rows, cols, vals = map(np.concatenate, (rows, cols, vals))
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+
+
+def _lfull(Ah, inF, partner, b11, b12, dg):
+    """L = A^_{C,F} B^{-1}, rows indexed by level index (C rows only)."""
+    n = Ah.shape[0]
+    Binv = _binv(n, inF, partner, b11, b12)
+    PF = sp.diags(inF.astype(float))
+    PC = sp.diags((~inF).astype(float))
+    Lf = sp.csr_matrix(PC @ Ah @ PF @ Binv)
+    Lf.eliminate_zeros()
+    return Lf
+
+
+class MultilevelILDL:
+    """M^{-1} ~ (A - sigma I)^{-1}; see module docstring."""
+
+    def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
+                 n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192):
+        self.levels = []
+        cur = sp.csr_matrix(A)
+        self.nnzA = cur.nnz
+        for lev in range(max_levels):
+            if cur.shape[0] <= n_coarse_max:
+                break
+            Lv = factor_level(cur, kappa, tau_drop, tau_strong,
+                              lattice_L if lev == 0 else None, stall_frac)
+            if Lv is None:
+                break
+            self.levels.append(Lv)
+            cur = Lv.S
+        if cur.shape[0] > dense_cap:
+            raise RuntimeError(f"multilevel ILDL breakdown: coarse size {cur.shape[0]} > {dense_cap}")
+        self.coarse_n = cur.shape[0]
+        if cur.shape[0] > 0:
+            G = np.linalg.inv(cur.toarray())
+            self.G = 0.5 * (G + G.T)
+        else:
+            self.G = np.zeros((0, 0))
+
+    def fill(self):
+        """nnz(LDL^T)/nnz(A) analogue: stored L entries + pivots + dense coarse triangle."""
+        nl = sum(Lv.L.nnz + len(Lv.F) + Lv.npairs for Lv in self.levels)
+        nc = self.coarse_n
+        return (nl + nc * (nc + 1) // 2) / self.nnzA
+
+    def apply(self, r):
+        return self._apply(np.asarray(r, dtype=np.float64), 0)
+
+    def _apply(self, r, lev):
+        if lev == len(self.levels):
+            return self.G @ r
+        Lv = self.levels[lev]
+        rh = Lv.D * r
+        wC = rh[Lv.C] - Lv.L @ rh
+        yC = self._apply(wC, lev + 1)
+        zh = np.empty_like(r)
+        zh[Lv.C] = yC
+        zF = Lv.Binv @ rh - Lv.L.T @ yC
+        zh[Lv.F] = zF[Lv.F]
+        return Lv.D * zh

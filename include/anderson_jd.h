@@ -1,0 +1,198 @@
+/*
+ * anderson_jd.h -- C ABI of the B200-native Anderson / Jacobi-Davidson hot path.
+ *
+ * Paper: O. Schenk, M. Bollhoefer, R. A. Roemer, "On large scale diagonalization
+ * techniques for the Anderson model of localization" (arxiv math/0508111),
+ * referenced below as PAPER.md with line numbers.
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers. A `d_` prefix means a device (HBM) pointer, `h_` a host
+ *     pointer.  Caller owns every buffer it passes; the library owns only the
+ *     opaque handles it returns (freed with the matching *_free call).
+ *   - Vectors of the lattice are fp64, length n = L^3, site s = i + L*(j + L*k)
+ *     (x fastest), periodic boundaries.
+ *   - Blocks of vectors are column-major with leading dimension n.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is enqueued on it; functions that return host results synchronise it.
+ *   - Return value: AJ_OK (0) or an AJ_ERR_* code; aj_last_error() returns a
+ *     thread-local human-readable message for the last failure.  No entry point
+ *     falls back to the CPU: without a usable sm_100a device they fail with
+ *     AJ_ERR_CUDA.
+ */
+#ifndef ANDERSON_JD_H
+#define ANDERSON_JD_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AJ_API __attribute__((visibility("default")))
+#else
+#define AJ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AJ_OK 0
+#define AJ_ERR_ARG 1        /* invalid argument (sizes, NULL pointers, L < 3) */
+#define AJ_ERR_CUDA 2       /* CUDA runtime / launch failure, no device      */
+#define AJ_ERR_BREAKDOWN 3  /* preconditioner or Krylov breakdown            */
+#define AJ_ERR_NOCONV 4     /* eigensolver hit max_outer before k pairs      */
+#define AJ_ERR_CAPACITY 5   /* internal capacity exceeded (see message)      */
+
+AJ_API const char* aj_last_error(void);
+/* Library version string, e.g. "anderson_jd 0.1 sm_100a". */
+AJ_API const char* aj_version(void);
+
+/* ------------------------------------------------------------------------- *
+ * anderson_build -- the disorder potential eps of Eq. (eigenequation)
+ * (PAPER.md l.182-193): eps_s ~ U[-W/2, W/2), s in [0, L^3).
+ * Generator (R3): SplitMix64 counter stream keyed by `seed`,
+ *   h_s = mix64(seed + (s+1)*0x9E3779B97F4A7C15), u_s = (h_s >> 11) * 2^-53,
+ *   eps_s = (u_s - 0.5) * W        (bit-exact, order independent).
+ * d_eps: device, n doubles, written.  Errors: AJ_ERR_ARG if L < 3 or W < 0.
+ * ------------------------------------------------------------------------- */
+AJ_API int anderson_build(double* d_eps, int32_t L, double W, uint64_t seed, void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * spmv -- y = (A - sigma I) x, matrix free (Eq.
+ * (eigenequation) l.182-186): (A x)_s = hop * sum_{6 periodic nbrs} x_nb + eps_s x_s.
+ * d_y, d_x, d_eps: device, n doubles; d_y must not alias d_x.
+ * ------------------------------------------------------------------------- */
+AJ_API int spmv(double* d_y, const double* d_x, const double* d_eps, int32_t L, double hop,
+         double sigma, void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * Symmetric multilevel incomplete LDL^T preconditioner K ~ A - sigma I
+ * (sect. 7, l.790-973), independent-set levels (DESIGN.md sect. 3.3):
+ * level 0 = red sites of the bipartite lattice, deeper levels = maximal
+ * independent sets of 1x1 / matched 2x2 pivots, inverse-based pivot bound
+ * ||L^{-1}||_inf <= kappa (l.884-897), dropping |l| < tau_drop (l.909-911),
+ * recursion on the Schur complement (l.917-945), dense coarse inverse.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  double kappa;          /* inverse bound, paper default 5    */
+  double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa)        */
+  double tau_strong;     /* strong-coupling threshold of the independent sets    */
+  int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
+  int32_t max_levels;    /* level cap                                            */
+  double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
+  int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN)      */
+  int32_t cand_cap;      /* per-row Schur candidate capacity (else CAPACITY)     */
+} aj_precond_params;
+
+typedef struct {
+  int32_t levels;         /* number of sparse levels                              */
+  int32_t coarse_n;       /* size of the dense coarse system                      */
+  int64_t nnz_L;          /* stored entries of all L factors                      */
+  int64_t nnz_A;          /* 7 n                                                  */
+  int32_t level_n[256];   /* size of each level                                   */
+  int32_t level_nF[256];  /* pivots eliminated at each level                      */
+  int32_t level_pairs[256]; /* 2x2 pivots at each level                           */
+  int64_t level_nnzS[256];  /* nnz of the Schur complement produced by each level */
+  double setup_ms;        /* device time of precond_setup                         */
+} aj_precond_info;
+
+AJ_API void aj_precond_default_params(aj_precond_params* p);
+
+/* handle: out, opaque; d_eps device n doubles (read during setup only). */
+AJ_API int precond_setup(void** handle, const double* d_eps, int32_t L, double hop, double sigma,
+                  const aj_precond_params* params, void* stream);
+/* z = K^{-1} r.  d_z, d_r: device n doubles, may not alias. Symmetric linear operator. */
+AJ_API int precond_apply(void* handle, double* d_z, const double* d_r, void* stream);
+AJ_API int precond_info(void* handle, aj_precond_info* info);
+AJ_API int precond_free(void* handle);
+
+/* ------------------------------------------------------------------------- *
+ * sqmr_solve -- simplified QMR for
+ * (A - sigma I) x = b with the preconditioner `handle` (NULL = identity).
+ * Stops when ||b - (A - sigma I) x|| <= tol ||b|| (recursive QMR residual,
+ * PAPER.md l.1094-1095) or after maxit steps.  d_x: out (zero start), d_b: in.
+ * h_iters / h_relres: out (host).  Returns AJ_ERR_BREAKDOWN on a Lanczos
+ * breakdown (q^T A q = 0 or rho = 0).
+ * ------------------------------------------------------------------------- */
+AJ_API int sqmr_solve(void* handle, double* d_x, const double* d_b, const double* d_eps, int32_t L,
+               double hop, double sigma, double tol, int32_t maxit, int32_t* h_iters,
+               double* h_relres, void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * Tall-skinny building blocks of the JD subspace work (DESIGN.md row 4).
+ * d_V: n x m column-major (ld = n).
+ * multi_dot:   h_out[m] = V^T x                       (fp64, deterministic order)
+ * ortho_cgs2:  x <- (I - V V^T)^2 x / ||.||, h_norm = norm before normalising
+ *              (V assumed orthonormal; 2-pass classical Gram-Schmidt).
+ * ------------------------------------------------------------------------- */
+AJ_API int multi_dot(double* h_out, const double* d_V, int32_t m, const double* d_x, int64_t n,
+              void* stream);
+AJ_API int ortho_cgs2(double* d_x, const double* d_V, int32_t m, int64_t n, double* h_norm,
+               void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * jd_solve -- the k eigenpairs of A nearest sigma by symmetric Jacobi-Davidson
+ * (sect. 4.2, l.380-421): Ritz extraction on V^T A V, correction
+ * equation (I-Q~Q~^T)(A-theta I)(I-Q~Q~^T) z = -r, Q~ = [Q, u], solved by SQMR
+ * with the projected preconditioner (I - Y H^{-1} Q~^T) K^{-1}, Y = K^{-1} Q~,
+ * H = Q~^T Y (the block form of (I - u w^T / w^T u) K^{-1}, l.414-416), K the
+ * multilevel ILDL at sigma; thick restart; deflation of converged pairs.
+ * Converged when ||A x - lambda x||_2 <= tol * ||A||_1, ||A||_1 = 6|hop| + max|eps|.
+ *
+ * d_eps: device n doubles.  h_lambda: host k (out, sorted by |lambda - sigma|).
+ * d_X: device n*k (out, orthonormal eigenvectors, may be NULL).
+ * h_resid: host k (out, ||A x - lambda x||_2 recomputed after convergence).
+ * Returns AJ_ERR_NOCONV (with the converged prefix filled) if max_outer is hit.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t jmin, jmax;    /* search space after restart / maximum                 */
+  int32_t max_outer;     /* outer iteration cap                                  */
+  int32_t inner_max;     /* SQMR steps per correction equation                   */
+  double inner_tol;      /* relative SQMR tolerance for the correction equation  */
+  double switch_tol;     /* use theta (not sigma) as shift once ||r|| < this*||A|| */
+  uint64_t seed;         /* start vector stream key                              */
+  int32_t verbose;       /* 1: per-outer log on stderr                           */
+} aj_jd_params;
+
+typedef struct {
+  int32_t outer, inner_total, converged, restarts;
+  double setup_ms, solve_ms, total_ms;
+  aj_precond_info precond;
+} aj_jd_stats;
+
+AJ_API void aj_jd_default_params(aj_jd_params* p);
+
+AJ_API int jd_solve(int32_t k, double sigma, double tol, const double* d_eps, int32_t L, double hop,
+             const aj_precond_params* pparams, const aj_jd_params* jparams, double* h_lambda,
+             double* d_X, double* h_resid, aj_jd_stats* stats, void* stream);
+
+/* Same, end to end from HOST buffers: h_eps (n doubles) is copied in, the
+ * eigenvectors are copied back into h_X (n*k doubles, may be NULL). */
+AJ_API int jd_solve_host(int32_t k, double sigma, double tol, const double* h_eps, int32_t L, double hop,
+                  const aj_precond_params* pparams, const aj_jd_params* jparams, double* h_lambda,
+                  double* h_X, double* h_resid, aj_jd_stats* stats, void* stream);
+
+/* Number of kernel launches issued by this thread since the last reset
+ * (bench accounting of "gpu_launches"). */
+AJ_API int64_t aj_launch_count(int32_t reset);
+
+/* ------------------------------------------------------------------------- *
+ * Live per-phase device timing (CUDA events recorded on the launching stream
+ * around each phase while enabled; used by bench.py for the roofline).
+ * Categories: 0 stencil SpMV (incl. fused dots), 1 preconditioner apply,
+ * 2 preconditioner setup, 3 SQMR vector updates, 4 JD subspace kernels.
+ * bytes = algorithmic HBM bytes of the recorded calls (DESIGN.md sect. 4).
+ * aj_prof_enable(1) resets and starts, (0) stops; aj_prof_get synchronises
+ * the device and returns the totals of this thread.
+ * ------------------------------------------------------------------------- */
+#define AJ_PROF_CATS 8
+typedef struct {
+  double ms[AJ_PROF_CATS];
+  double bytes[AJ_PROF_CATS];
+  int64_t calls[AJ_PROF_CATS];
+} aj_prof;
+AJ_API int aj_prof_enable(int32_t on);
+AJ_API int aj_prof_get(aj_prof* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANDERSON_JD_H */

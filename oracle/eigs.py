@@ -34,17 +34,22 @@ def dense_nearest(A, k, sigma=0.0):
     return lam[idx], X[:, idx]
 
 
-def si_lanczos_nearest(A, k, sigma=0.0, tol=1e-12, m0=None, mmax=600, seed=12345):
+def si_lanczos_nearest(A, k, sigma=0.0, tol=1e-12, m0=None, mmax=600, seed=12345, solve=None):
     """k eigenpairs of sparse symmetric A nearest sigma via plain
     shift-and-invert Lanczos (sect. 4.1) with full reorthogonalisation.
 
     Grows the Krylov dimension m (no implicit restart) until the k wanted
     Ritz pairs satisfy ||A x - lambda x|| <= tol * ||A||_1.
+    solve: callable v -> (A - sigma I)^{-1} v to full accuracy; default a sparse
+    direct LU (fine up to L ~ 20; SuperLU fill explodes on 3-D lattices beyond,
+    see `iterative_solver`).
     Returns (lam[k], X[n,k], resid[k])."""
     A = sp.csr_matrix(A)
     n = A.shape[0]
     normA = abs(A).sum(axis=0).max()
-    lu = spl.splu(sp.csc_matrix(A - sigma * sp.identity(n)))
+    if solve is None:
+        lu = spl.splu(sp.csc_matrix(A - sigma * sp.identity(n)))
+        solve = lu.solve
     rng = np.random.default_rng(seed)
     v = rng.standard_normal(n)
     V = [v / np.linalg.norm(v)]
@@ -54,7 +59,7 @@ def si_lanczos_nearest(A, k, sigma=0.0, tol=1e-12, m0=None, mmax=600, seed=12345
     scale = 0.0
     while True:
         while len(alpha) < m:
-            w = lu.solve(V[-1])
+            w = solve(V[-1])
             a = V[-1] @ w
             w = w - a * V[-1] - (beta[-1] * V[-2] if beta else 0.0)
             Vm = np.array(V)
@@ -80,3 +85,26 @@ def si_lanczos_nearest(A, k, sigma=0.0, tol=1e-12, m0=None, mmax=600, seed=12345
         if np.all(res[idx] <= tol * normA) or len(alpha) >= mmax or beta[-1] == 0.0:
             return lam[idx], X[:, idx], res[idx]
         m = min(mmax, int(m * 1.5))
+
+
+def iterative_solver(A, sigma, L=None, tol=1e-14, maxit=2000):
+    """(A - sigma I)^{-1} v "to full accuracy" by oracle SQMR
+    preconditioned with the oracle multilevel ILDL (reading R14), for lattices
+    where a sparse direct LU is out of reach.  Raises if an inner solve stalls
+    above 100*tol."""
+    from .mlildl import MultilevelILDL
+    from .sqmr import sqmr
+    As = sp.csr_matrix(A - sigma * sp.identity(A.shape[0]))
+    M = MultilevelILDL(As, lattice_L=L, n_coarse_max=1024)
+    stats = {"solves": 0, "iters": 0}
+
+    def solve(v):
+        x, it, res, _ = sqmr(lambda q: As @ q, M.apply, v, tol=tol, maxit=maxit)
+        if not res <= 100 * tol:
+            raise RuntimeError(f"inner solve stalled at {res:.2e}")
+        stats["solves"] += 1
+        stats["iters"] += it
+        return x
+
+    solve.stats = stats
+    return solve

@@ -106,7 +106,7 @@ def _pair_candidates(Ah, dg, lmax1, d1, p, kappa):
         rj = Ah.getrow(j).tocoo()
         ai = dict(zip(ri.col.tolist(), ri.data.tolist()))
         aj = dict(zip(rj.col.tolist(), rj.data.tolist()))
-        nbrs = (set(ai) | set(aj)) - {i, j}
+        nbrs = sorted((set(ai) | set(aj)) - {i, j})
         lm2, d2 = 0.0, 0.0
         for cc in nbrs:
             aci, acj = ai.get(cc, 0.0), aj.get(cc, 0.0)
@@ -250,24 +250,67 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
     # L stored with rows = coarse index, cols = level index (F nodes)
     Lv.L = sp.csr_matrix((Lc.data[keep], (cmap[Lc.row[keep]], Lc.col[keep])), shape=(len(Lv.C), n))
     Lv.L.sort_indices()
-    Binv = _binv(n, inF, partner, b11, b12)
-    AhCF = Ah[Lv.C][:, Lv.F]
-    S = Ah[Lv.C][:, Lv.C] - AhCF @ Binv[Lv.F][:, Lv.F] @ AhCF.T
-    S = sp.csr_matrix(S)
-    S = 0.5 * (S + S.T)                           # exact symmetry (reading R10)
-    S = S.tocoo()
-    keepS = (S.row == S.col) | (np.abs(S.data) >= tau_drop)
-    nC = len(Lv.C)
-    S = sp.csr_matrix((S.data[keepS], (S.row[keepS], S.col[keepS])), shape=(nC, nC))
-    # explicit diagonal even when zero
-    dS = S.diagonal()
-    S = S + sp.csr_matrix((np.zeros(nC), (np.arange(nC), np.arange(nC))), shape=(nC, nC))
-    S = sp.csr_matrix(S)
-    S.sort_indices()
-    assert np.array_equal(S.diagonal(), dS)
-    Lv.S = S
-    Lv.Binv = Binv
+    Lv.S = _schur(Ah, inF, partner, b11, b12, Lv.C, cmap, tau_drop)
+    Lv.Binv = _binv(n, inF, partner, b11, b12)
     return Lv
+
+
+def _schur(Ah, inF, partner, b11, b12, C, cmap, tau_drop):
+    """S = A^_CC - A^_CF B^{-1} A^_FC, reading R10:
+    s_cc' = a^_cc' - sum_{blocks b adjacent to c and c', ascending leader} T_b(c, c') with
+      1x1 {f}:    T = B_ff (a_cf a_c'f)
+      2x2 {f,g}:  T = (B_ff (a_cf a_c'f) + B_gg (a_cg a_c'g)) + B_fg ((a_cf a_c'g) + (a_cg a_c'f))
+    (symmetric in c, c' term by term), then off-diagonals |s| < tau_drop dropped."""
+    n = Ah.shape[0]
+    nC = len(C)
+    coo = Ah.tocoo()
+    r, c, v = coo.row, coo.col, coo.data
+    # entries (c in C, u in F): block leader f = min(u, partner), value to f / to g
+    m = (~inF[r]) & inF[c]
+    rc, uc, av = r[m], c[m], v[m]
+    lead = np.where(partner[uc] >= 0, np.minimum(uc, partner[uc]), uc)
+    key = rc * n + lead
+    uk, inv = np.unique(key, return_inverse=True)
+    acf = np.zeros(len(uk))
+    acg = np.zeros(len(uk))
+    isf = uc == lead
+    acf[inv[isf]] = av[isf]
+    acg[inv[~isf]] = av[~isf]
+    ec, el = uk // n, uk % n                         # element = (C row, block leader)
+    o = np.lexsort((ec, el))                         # group by leader
+    ec, el, acf, acg = ec[o], el[o], acf[o], acg[o]
+    gstart = np.flatnonzero(np.r_[True, el[1:] != el[:-1]])
+    gcnt = np.diff(np.r_[gstart, len(el)])
+    gid = np.repeat(np.arange(len(gstart)), gcnt)
+    E = len(el)
+    reps = gcnt[gid]
+    a_idx = np.repeat(np.arange(E), reps)
+    before = np.repeat(np.cumsum(reps) - reps, reps)
+    b_idx = gstart[gid[a_idx]] + (np.arange(len(a_idx)) - before)
+    f = el[a_idx]
+    g = partner[f]
+    Bff = b11[f]
+    A1, A2 = acf[a_idx], acf[b_idx]
+    G1, G2 = acg[a_idx], acg[b_idx]
+    T = Bff * (A1 * A2)
+    pm = g >= 0
+    gg = g[pm]
+    T[pm] = (Bff[pm] * (A1[pm] * A2[pm]) + b11[gg] * (G1[pm] * G2[pm])) + \
+        b12[f[pm]] * ((A1[pm] * G2[pm]) + (G1[pm] * A2[pm]))
+    tk = cmap[ec[a_idx]] * nC + cmap[ec[b_idx]]
+    # starting values a^_cc' on C x C (diagonal always present)
+    mc = (~inF[r]) & (~inF[c])
+    k0 = cmap[r[mc]] * nC + cmap[c[mc]]
+    keys = np.unique(np.concatenate([k0, tk, np.arange(nC) * (nC + 1)]))
+    sval = np.zeros(len(keys))
+    sval[np.searchsorted(keys, k0)] = v[mc]
+    ot = np.lexsort((f, tk))                         # per entry: ascending leader
+    np.subtract.at(sval, np.searchsorted(keys, tk[ot]), T[ot])
+    sr, sc = keys // nC, keys % nC
+    keep = (sr == sc) | (np.abs(sval) >= tau_drop)
+    S = sp.csr_matrix((sval[keep], (sr[keep], sc[keep])), shape=(nC, nC))
+    S.sort_indices()
+    return S
 
 
 def _binv(n, inF, partner, b11, b12):

@@ -1,0 +1,51 @@
+// Internal launch interfaces of the Anderson JD library.
+#pragma once
+#include "aj_common.cuh"
+
+namespace aj {
+
+// Reduction scratch shared by the fused-reduction kernels of one solve.
+// partials: kMaxPartials doubles; tickets: kMaxTickets zero-initialised counters.
+constexpr int kMaxPartials = 148 * 64 * 80;
+constexpr int kMaxTickets = 64;
+struct RedScratch {
+  double* partials = nullptr;
+  unsigned* tickets = nullptr;
+  void init(cudaStream_t s);
+  void release(cudaStream_t s);
+  RedBuf buf(double* out, int ticket = 0) const { return RedBuf{partials, tickets + ticket, out}; }
+};
+
+// --- lattice (aj_stencil.cu) ---
+void launch_disorder(double* eps, int L, double W, uint64_t seed, cudaStream_t st);
+void launch_spmv(double* y, const double* x, const double* eps, int L, double hop, double sig,
+                 cudaStream_t st);
+// y = (A - sig I) x and out[c] = <y, W_c>, c < nv (nv <= 10) via rb (fused reduction)
+void launch_spmv_dots(double* y, const double* x, const double* eps, int L, double hop, double sig,
+                      const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st);
+int spmv_grid_blocks(int L);
+
+// --- tall skinny (aj_blas.cu) ---
+// out[0..m) = V^T x   (out device, padded to a multiple of 8)
+void launch_multi_dot(double* out, const double* V, int m, int64_t ld, const double* x, int64_t n,
+                      const RedScratch& rs, cudaStream_t st);
+// y = beta*y + alpha * V c      (c device, m <= 64; y may not alias V)
+void launch_gemv(double* y, double beta, double alpha, const double* V, int m, int64_t ld,
+                 const double* c, int64_t n, cudaStream_t st);
+// O[:, 0..q) = V[:, 0..p) S   (S device col-major p x q, lds = p; O may not alias V)
+void launch_gemm_ts(double* O, int64_t ldo, const double* V, int p, int64_t ldv, const double* S,
+                    int q, int64_t n, cudaStream_t st);
+// out[0] = <x, y>
+void launch_dot(double* out, const double* x, const double* y, int64_t n, const RedScratch& rs,
+                cudaStream_t st);
+// y = a*x + b*y
+void launch_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t st);
+// x *= 1/sqrt(*nrm2)  (nrm2 device scalar holding ||x||^2)
+void launch_normalize(double* x, const double* nrm2, int64_t n, cudaStream_t st);
+void launch_copy(double* y, const double* x, int64_t n, cudaStream_t st);
+void launch_fill(double* y, double v, int64_t n, cudaStream_t st);
+
+void prof_enable(bool on);
+void prof_get(aj_prof* out);
+
+}  // namespace aj

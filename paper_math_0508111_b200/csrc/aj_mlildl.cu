@@ -1,0 +1,1224 @@
+// Symmetric multilevel incomplete LDL^T preconditioner on the GPU.
+//
+// PAPER.md sect. 7 (l.790-973): per level (i) symmetric scaling (l.805-807),
+// (ii) 1x1 / matched 2x2 pivots with the d1/d2 test (l.864-874) and the
+// inverse-based bound ||L^{-1}|| <= kappa with postponement (l.884-897),
+// (iii) L = A_CF B^{-1} with dropping |l| < tau_drop (l.909-911), explicit
+// Schur complement of the postponed nodes (l.940-945), recursion, dense coarse.
+// The levels are realised as INDEPENDENT SETS (DESIGN.md sect. 3.3): level 0
+// is the red half of the bipartite lattice, deeper levels maximal independent
+// sets of pivot blocks in the strong graph, so every step -- scaling, pivot
+// tests, independent-set rounds, budget repair, L/L^T/S construction and the
+// forward/backward application -- is a level-parallel kernel over rows.
+//
+// Data layout (HBM): every level matrix is CSR (int64 row pointers, int32
+// sorted column indices, fp64 values, explicit diagonal).  Per level the
+// factor keeps L (rows = coarse nodes, cols = level index, values L_cf*D_f)
+// and L^T (rows = level nodes, cols = coarse index, values L_cf) so both
+// substitutions are pure gathers (no atomics).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "aj_common.cuh"
+#include "aj_kernels.cuh"
+#include "aj_mlildl.cuh"
+
+namespace aj {
+
+constexpr int TB = 256;
+static int grid_for(int64_t n) { return std::max(1, ceil_div(n, TB)); }
+
+// ----------------------------------------------------------------------------
+// level-0 CSR of A - sigma I on the lattice (7 sorted entries per row)
+__global__ void k_lattice_csr(int L, const double* __restrict__ eps, double hop, double sigma,
+                              int64_t* __restrict__ ptr, int32_t* __restrict__ col,
+                              double* __restrict__ val) {
+  const int64_t n = (int64_t)L * L * L;
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    const int i = (int)(s % L), j = (int)((s / L) % L), k = (int)(s / ((int64_t)L * L));
+    int32_t c[7];
+    c[0] = (int32_t)s;
+    c[1] = (int32_t)(((i + L - 1) % L) + (int64_t)L * (j + (int64_t)L * k));
+    c[2] = (int32_t)(((i + 1) % L) + (int64_t)L * (j + (int64_t)L * k));
+    c[3] = (int32_t)(i + (int64_t)L * (((j + L - 1) % L) + (int64_t)L * k));
+    c[4] = (int32_t)(i + (int64_t)L * (((j + 1) % L) + (int64_t)L * k));
+    c[5] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + L - 1) % L)));
+    c[6] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + 1) % L)));
+    for (int a = 1; a < 7; ++a) {  // insertion sort
+      int32_t v = c[a];
+      int b = a - 1;
+      while (b >= 0 && c[b] > v) {
+        c[b + 1] = c[b];
+        --b;
+      }
+      c[b + 1] = v;
+    }
+    ptr[s] = 7 * s;
+    if (s == n - 1) ptr[n] = 7 * n;
+    for (int a = 0; a < 7; ++a) {
+      col[7 * s + a] = c[a];
+      val[7 * s + a] = (c[a] == (int32_t)s) ? (eps[s] - sigma) : hop;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// (i) scaling D_i = 1/sqrt(max_j |a_ij|); scaled values a^_ij = a_ij * (D_i D_j)
+__global__ void k_rowmax_scale(int n, const int64_t* __restrict__ ptr, const double* __restrict__ val,
+                               double* __restrict__ D) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    double m = 0.0;
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) m = fmax(m, fabs(val[e]));
+    D[i] = (m > 0.0) ? 1.0 / sqrt(m) : 1.0;
+  }
+}
+
+// scaled values + per-row pivot quality:
+//   dg = a^_ii, lmax1 = max_{j!=i}|a^_ij| / |a^_ii|, d1 = sum_{j!=i}|a^_ij| / |a^_ii|,
+//   p = argmax_{j!=i} |a^_ij| (ties -> smallest j; rows are column sorted)
+__global__ void k_scaled_quality(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, const double* __restrict__ D,
+                                 double* __restrict__ ah, double* __restrict__ dg,
+                                 double* __restrict__ lmax1, double* __restrict__ d1,
+                                 int32_t* __restrict__ prop, int8_t* __restrict__ ok1, double kappa) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const double Di = D[i];
+    double diag = 0.0, cm = 0.0, os = 0.0;
+    int32_t p = -1;
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+      const int32_t j = col[e];
+      const double v = val[e] * (Di * D[j]);
+      ah[e] = v;
+      if (j == i) {
+        diag = v;
+      } else {
+        const double a = fabs(v);
+        os += a;
+        if (a > cm) {
+          cm = a;
+          p = j;
+        }
+      }
+    }
+    const double ad = fabs(diag);
+    dg[i] = diag;
+    const double l1 = (ad > 0.0) ? cm / ad : INFINITY;
+    lmax1[i] = l1;
+    d1[i] = (ad > 0.0) ? os / ad : INFINITY;
+    prop[i] = p;
+    ok1[i] = (l1 <= kappa - 1.0 && diag != 0.0) ? 1 : 0;
+  }
+}
+
+// position of column `key` in the sorted row [lo,hi), or -1
+__device__ __forceinline__ int64_t lookup_idx(const int32_t* __restrict__ col, int64_t lo, int64_t hi,
+                                              int32_t key) {
+  int64_t a = lo, b = hi;
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if (col[mid] < key)
+      a = mid + 1;
+    else
+      b = mid;
+  }
+  return (a < hi && col[a] == key) ? a : -1;
+}
+
+// returns a^_{row,key} or 0 (sorted row [lo,hi))
+__device__ __forceinline__ double lookup(const int32_t* __restrict__ col, const double* __restrict__ ah,
+                                         int64_t lo, int64_t hi, int32_t key) {
+  int64_t a = lo, b = hi;
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if (col[mid] < key)
+      a = mid + 1;
+    else
+      b = mid;
+  }
+  return (a < hi && col[a] == key) ? ah[a] : 0.0;
+}
+
+// l_cu for member u of a block {f} or {f, g} (f < g) from the row values
+// a_cf, a_cg (0 if absent): l_cu = sum_{v in block, ascending} a_cv * Binv[v,u]
+// (the summation order of oracle/mlildl.py's sparse product).
+__device__ __forceinline__ double lval_pair(double a_cf, double a_cg, double Bvu_f, double Bvu_g) {
+  return __dadd_rn(__dmul_rn(a_cf, Bvu_f), __dmul_rn(a_cg, Bvu_g));
+}
+
+// (ii-a) 2x2 candidates: mutual strongest-neighbour proposals (sect. 6.2), d2 < d1_lead
+// and lmax2 <= kappa - 1 (sect. 7.2).  Thread i handles the pair {i, p(i)} when i < p(i).
+__global__ void k_pairs(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ ah, const double* __restrict__ dg,
+                        const double* __restrict__ d1, const int32_t* __restrict__ prop,
+                        const int8_t* __restrict__ ok1, double kappa, int32_t* __restrict__ partner,
+                        double* __restrict__ b11, double* __restrict__ b12, double* __restrict__ q,
+                        int* __restrict__ npairs) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t j = prop[i];
+    if (j <= i || prop[j] != i) continue;
+    if (ok1[i] && ok1[j]) continue;
+    const double aii = dg[i], ajj = dg[j];
+    const double aij = lookup(col, ah, ptr[i], ptr[i + 1], j);
+    const double det = __dsub_rn(__dmul_rn(aii, ajj), __dmul_rn(aij, aij));
+    if (det == 0.0) continue;
+    const double B11 = ajj / det, B12 = -aij / det, B22 = aii / det;
+    // merge rows i and j (both sorted) over neighbours c not in {i, j}
+    int64_t ei = ptr[i], ej = ptr[j];
+    const int64_t ei1 = ptr[i + 1], ej1 = ptr[j + 1];
+    double lm2 = 0.0, d2 = 0.0;
+    while (ei < ei1 || ej < ej1) {
+      const int32_t ci = (ei < ei1) ? col[ei] : INT32_MAX;
+      const int32_t cj = (ej < ej1) ? col[ej] : INT32_MAX;
+      const int32_t c = min(ci, cj);
+      double aci = 0.0, acj = 0.0;
+      if (ci == c) aci = ah[ei++];
+      if (cj == c) acj = ah[ej++];
+      if (c == i || c == j) continue;
+      // (l_ci, l_cj) = (a_ci, a_cj) B^{-1}; i < j
+      const double w = fabs(lval_pair(aci, acj, B11, B12)) + fabs(lval_pair(aci, acj, B12, B22));
+      lm2 = fmax(lm2, w);
+      d2 += w;
+    }
+    const int lead = ok1[i] ? j : i;
+    if (d2 < d1[lead] && lm2 <= kappa - 1.0) {
+      partner[i] = j;
+      partner[j] = i;
+      b11[i] = B11;
+      b12[i] = B12;
+      b11[j] = B22;
+      b12[j] = B12;
+      q[i] = lm2;
+      atomicAdd(npairs, 1);
+    }
+  }
+}
+
+// (ii-b) blocks: singles (ok1, unpaired) and pair leaders; red-set selection on level 0
+__global__ void k_blocks(int n, int L, const int8_t* __restrict__ ok1, const double* __restrict__ dg,
+                         const double* __restrict__ lmax1, const int32_t* __restrict__ partner,
+                         int32_t* __restrict__ leader, double* __restrict__ q, double* __restrict__ b11,
+                         int8_t* __restrict__ inF) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t p = partner[i];
+    if (p >= 0) {
+      leader[i] = min(i, p);
+    } else if (ok1[i]) {
+      leader[i] = i;
+      q[i] = lmax1[i];
+      b11[i] = 1.0 / dg[i];
+    } else {
+      leader[i] = -1;
+    }
+    if (L > 0) {  // level 0: red sites of the bipartite split (reading R6)
+      const int x = i % L, y = (i / L) % L, z = i / (L * L);
+      bool red = ((x + y + z) & 1) == 0;
+      if (L & 1) red = red && x < L - 1 && y < L - 1 && z < L - 1;
+      inF[i] = (p < 0 && ok1[i] && red) ? 1 : 0;
+    }
+  }
+}
+
+// MIS rank keys: key = bits(q) for block leaders (q >= 0), else max
+__global__ void k_rank_keys(int n, const int32_t* __restrict__ leader, const double* __restrict__ q,
+                            uint64_t* __restrict__ key, int32_t* __restrict__ idx) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    key[i] = (leader[i] == i) ? (uint64_t)__double_as_longlong(q[i]) : ~0ull;
+    idx[i] = i;
+  }
+}
+__global__ void k_rank_scatter(int n, const int32_t* __restrict__ sorted_idx, int32_t* __restrict__ rank) {
+  for (int t = blockIdx.x * TB + threadIdx.x; t < n; t += gridDim.x * TB) rank[sorted_idx[t]] = t;
+}
+
+// status per block (at leader): 0 undecided, 1 selected, 2 removed
+__global__ void k_mis_nbmin(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                            const double* __restrict__ ah, double tau_s, const int32_t* __restrict__ leader,
+                            const int8_t* __restrict__ status, const int32_t* __restrict__ rank,
+                            int32_t* __restrict__ nbmin) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t l = leader[i];
+    if (l < 0 || status[l] != 0) continue;
+    int32_t m = INT32_MAX;
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+      const int32_t j = col[e];
+      if (j == i || !(fabs(ah[e]) >= tau_s)) continue;
+      const int32_t lj = leader[j];
+      if (lj < 0 || lj == l || status[lj] != 0) continue;
+      m = min(m, rank[lj]);
+    }
+    nbmin[i] = m;
+  }
+}
+__global__ void k_mis_win(int n, const int32_t* __restrict__ leader, const int32_t* __restrict__ partner,
+                          const int8_t* __restrict__ status, const int32_t* __restrict__ rank,
+                          const int32_t* __restrict__ nbmin, int8_t* __restrict__ win) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    if (leader[i] != i || status[i] != 0) continue;
+    int32_t m = nbmin[i];
+    if (partner[i] >= 0) m = min(m, nbmin[partner[i]]);
+    if (rank[i] < m) win[i] = 1;
+  }
+}
+__global__ void k_mis_remove(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                             const double* __restrict__ ah, double tau_s, const int32_t* __restrict__ leader,
+                             const int8_t* __restrict__ status, const int8_t* __restrict__ win,
+                             int8_t* __restrict__ rem) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t l = leader[i];
+    if (l < 0 || status[l] != 0 || win[l]) continue;
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+      const int32_t j = col[e];
+      if (j == i || !(fabs(ah[e]) >= tau_s)) continue;
+      const int32_t lj = leader[j];
+      if (lj >= 0 && lj != l && win[lj]) {
+        rem[l] = 1;
+        break;
+      }
+    }
+  }
+}
+__global__ void k_mis_apply(int n, const int32_t* __restrict__ leader, int8_t* __restrict__ status,
+                            int8_t* __restrict__ win, int8_t* __restrict__ rem, int* __restrict__ undecided) {
+  int cnt = 0;
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    if (leader[i] != i || status[i] != 0) continue;
+    if (win[i])
+      status[i] = 1;
+    else if (rem[i])
+      status[i] = 2;
+    else
+      ++cnt;
+    win[i] = 0;
+    rem[i] = 0;
+  }
+  if (cnt) atomicAdd(undecided, cnt);
+}
+__global__ void k_mis_final(int n, const int32_t* __restrict__ leader, const int8_t* __restrict__ status,
+                            int8_t* __restrict__ inF) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t l = leader[i];
+    inF[i] = (l >= 0 && status[l] == 1) ? 1 : 0;
+  }
+}
+
+// Iterate the F blocks adjacent to row c (c not in F) and call fn(f, g, l_cf, l_cg, lead)
+// once per block; g = -1 for singles.  Order: ascending position in row c of the
+// first adjacent member.
+template <typename Fn>
+__device__ __forceinline__ void for_blocks_of_row(int c, const int64_t* __restrict__ ptr,
+                                                  const int32_t* __restrict__ col,
+                                                  const double* __restrict__ ah,
+                                                  const int8_t* __restrict__ inF,
+                                                  const int32_t* __restrict__ partner,
+                                                  const double* __restrict__ b11,
+                                                  const double* __restrict__ b12, Fn fn) {
+  const int64_t lo = ptr[c], hi = ptr[c + 1];
+  for (int64_t e = lo; e < hi; ++e) {
+    const int32_t u = col[e];
+    if (u == c || !inF[u]) continue;
+    const int32_t p = partner[u];
+    if (p < 0) {
+      fn(u, -1, __dmul_rn(ah[e], b11[u]), 0.0, u);
+    } else {
+      // handle the pair once: at the smaller adjacent member
+      const int64_t ep = lookup_idx(col, lo, hi, p);
+      if (ep >= 0 && p < u) continue;
+      const double a_cp = (ep >= 0) ? ah[ep] : 0.0;
+      const int32_t f = min(u, p), g = max(u, p);
+      const double a_cf = (f == u) ? ah[e] : a_cp;
+      const double a_cg = (g == u) ? ah[e] : a_cp;
+      // l_cf = a_cf Binv[f,f] + a_cg Binv[g,f]; l_cg = a_cf Binv[f,g] + a_cg Binv[g,g]
+      const double lf = lval_pair(a_cf, a_cg, b11[f], b12[g]);
+      const double lg = lval_pair(a_cf, a_cg, b12[f], b11[g]);
+      fn(f, g, lf, lg, f);
+    }
+  }
+}
+
+// (ii-c) row-budget repair: rows of L^{-1} bounded, sum_b w_cb <= kappa - 1;
+// a violating row nominates its largest block (ties -> smallest leader).
+__global__ void k_budget(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                         const double* __restrict__ ah, const int8_t* __restrict__ inF,
+                         const int32_t* __restrict__ partner, const double* __restrict__ b11,
+                         const double* __restrict__ b12, double kappa, int8_t* __restrict__ nominate,
+                         int* __restrict__ nviol) {
+  for (int c = blockIdx.x * TB + threadIdx.x; c < n; c += gridDim.x * TB) {
+    if (inF[c]) continue;
+    double budget = 0.0, wbest = -1.0;
+    int32_t lbest = INT32_MAX;
+    for_blocks_of_row(c, ptr, col, ah, inF, partner, b11, b12,
+                      [&](int32_t f, int32_t g, double lf, double lg, int32_t lead) {
+                        const double w = fabs(lf) + (g >= 0 ? fabs(lg) : 0.0);
+                        budget += w;
+                        if (w > wbest || (w == wbest && lead < lbest)) {
+                          wbest = w;
+                          lbest = lead;
+                        }
+                      });
+    if (budget > kappa - 1.0) {
+      nominate[lbest] = 1;
+      atomicAdd(nviol, 1);
+    }
+  }
+}
+__global__ void k_budget_apply(int n, const int32_t* __restrict__ partner, int8_t* __restrict__ inF,
+                               int8_t* __restrict__ nominate) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    if (!inF[i]) continue;
+    const int32_t p = partner[i];
+    const int32_t l = (p >= 0) ? min(i, p) : i;
+    if (nominate[l]) inF[i] = 0;
+  }
+}
+__global__ void k_clear_nominate(int n, const int32_t* __restrict__ partner, const int8_t* __restrict__ inF,
+                                 int8_t* __restrict__ nominate, int* __restrict__ nF, int* __restrict__ npairsF) {
+  int cf = 0, cp = 0;
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    nominate[i] = 0;
+    if (inF[i]) {
+      ++cf;
+      if (partner[i] > i) ++cp;
+    }
+  }
+  if (cf) atomicAdd(nF, cf);
+  if (cp) atomicAdd(npairsF, cp);
+}
+
+// (iii) compaction helpers
+__global__ void k_cflags(int n, const int8_t* __restrict__ inF, int32_t* __restrict__ flag) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) flag[i] = inF[i] ? 0 : 1;
+}
+__global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __restrict__ scan,
+                       int32_t* __restrict__ cmap, int32_t* __restrict__ cidx,
+                       int32_t* __restrict__ partner_out, const int32_t* __restrict__ partner,
+                       double* __restrict__ b11, double* __restrict__ b12) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    if (inF[i]) {
+      cmap[i] = -1;
+      partner_out[i] = partner[i];
+    } else {
+      cmap[i] = scan[i];
+      cidx[scan[i]] = i;
+      partner_out[i] = -1;
+      b11[i] = 0.0;
+      b12[i] = 0.0;
+    }
+  }
+}
+
+// L rows (coarse c'): entries (u, l_cu * D_u) with |l_cu| >= tau_drop
+template <bool FILL>
+__global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t* __restrict__ ptr,
+                         const int32_t* __restrict__ col, const double* __restrict__ ah,
+                         const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
+                         const double* __restrict__ b11, const double* __restrict__ b12,
+                         const double* __restrict__ D, double tau, int64_t* __restrict__ cnt_or_ptr,
+                         int32_t* __restrict__ Lcol, double* __restrict__ Lval) {
+  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
+    const int c = cidx[cp];
+    int64_t w = FILL ? cnt_or_ptr[cp] : 0;
+    for_blocks_of_row(c, ptr, col, ah, inF, partner, b11, b12,
+                      [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
+                        if (fabs(lf) >= tau) {
+                          if (FILL) {
+                            Lcol[w] = f;
+                            Lval[w] = lf * D[f];
+                          }
+                          ++w;
+                        }
+                        if (g >= 0 && fabs(lg) >= tau) {
+                          if (FILL) {
+                            Lcol[w] = g;
+                            Lval[w] = lg * D[g];
+                          }
+                          ++w;
+                        }
+                      });
+    if (!FILL) cnt_or_ptr[cp] = w;
+  }
+}
+
+// L^T rows (F node u): entries (cmap[c], l_cu) over C nodes c adjacent to u or its partner
+template <bool FILL>
+__global__ void k_LT_rows(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                          const double* __restrict__ ah, const int8_t* __restrict__ inF,
+                          const int32_t* __restrict__ partner, const double* __restrict__ b11,
+                          const double* __restrict__ b12, const int32_t* __restrict__ cmap, double tau,
+                          int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ LTcol,
+                          double* __restrict__ LTval) {
+  for (int u = blockIdx.x * TB + threadIdx.x; u < n; u += gridDim.x * TB) {
+    int64_t w = FILL ? cnt_or_ptr[u] : 0;
+    if (inF[u]) {
+      const int32_t p = partner[u];
+      if (p < 0) {
+        for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+          const int32_t c = col[e];
+          if (c == u || inF[c]) continue;
+          const double l = __dmul_rn(ah[e], b11[u]);
+          if (fabs(l) >= tau) {
+            if (FILL) {
+              LTcol[w] = cmap[c];
+              LTval[w] = l;
+            }
+            ++w;
+          }
+        }
+      } else {
+        const int32_t f = min(u, p), g = max(u, p);
+        int64_t ef = ptr[f], eg = ptr[g];
+        const int64_t ef1 = ptr[f + 1], eg1 = ptr[g + 1];
+        while (ef < ef1 || eg < eg1) {
+          const int32_t cf = (ef < ef1) ? col[ef] : INT32_MAX;
+          const int32_t cg = (eg < eg1) ? col[eg] : INT32_MAX;
+          const int32_t c = min(cf, cg);
+          double a_cf = 0.0, a_cg = 0.0;
+          if (cf == c) a_cf = ah[ef++];
+          if (cg == c) a_cg = ah[eg++];
+          if (c == f || c == g || inF[c]) continue;
+          const double l = (u == f) ? lval_pair(a_cf, a_cg, b11[f], b12[g])
+                                    : lval_pair(a_cf, a_cg, b12[f], b11[g]);
+          if (fabs(l) >= tau) {
+            if (FILL) {
+              LTcol[w] = cmap[c];
+              LTval[w] = l;
+            }
+            ++w;
+          }
+        }
+      }
+    }
+    if (!FILL) cnt_or_ptr[u] = w;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, symmetric by construction,
+// off-diagonals with |s| < tau dropped.  One warp per coarse row.
+constexpr int SW = 4;           // warps per CTA
+constexpr int BMAX = 96;        // F blocks adjacent to one row
+constexpr int HT = 4096;        // per-warp hash set of candidate columns (power of 2)
+struct BlkEnt {
+  int32_t f, g, lead;
+  double acf, acg, Bff, Bgg, Bfg;
+};
+constexpr size_t kSchurSmem = (size_t)SW * (HT * sizeof(int32_t) + BMAX * sizeof(BlkEnt));
+
+__device__ __forceinline__ void warp_bitonic_sort(int32_t* a, int P) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < P; t += 32) {
+        const int ixj = t ^ j;
+        if (ixj > t) {
+          const int32_t x = a[t], y = a[ixj];
+          const bool up = (t & k) == 0;
+          if ((x > y) == up) {
+            a[t] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// insert key into the warp's open-addressing set; counts new keys in *cnt
+__device__ __forceinline__ void hset_insert(int32_t* tab, int32_t key, int* cnt) {
+  uint32_t h = ((uint32_t)key * 2654435761u) & (HT - 1);
+  for (int probe = 0; probe < HT; ++probe) {
+    const int32_t prev = atomicCAS(&tab[h], -1, key);
+    if (prev == -1) {
+      atomicAdd(cnt, 1);
+      return;
+    }
+    if (prev == key) return;
+    h = (h + 1) & (HT - 1);
+  }
+}
+
+// Schur complement S = A^_CC - A^_CF B^{-1} A^_FC (reading R10: ascending-leader
+// accumulation of the symmetric block terms, bitwise symmetric), off-diagonals
+// with |s| < tau dropped.  One warp per coarse row.
+template <bool FILL>
+__global__ void __launch_bounds__(SW * 32)
+    k_schur(int nC, const int32_t* __restrict__ cidx, const int32_t* __restrict__ cmap,
+            const int64_t* __restrict__ ptr, const int32_t* __restrict__ col, const double* __restrict__ ah,
+            const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
+            const double* __restrict__ b11, const double* __restrict__ b12, double tau,
+            int32_t* __restrict__ scratch_all, int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ Scol,
+            double* __restrict__ Sval, int* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int scount[SW], sbcount[SW], sccount[SW];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (size_t)wid * HT;
+  BlkEnt* blk = reinterpret_cast<BlkEnt*>(smem_raw + (size_t)SW * HT * sizeof(int32_t)) + (size_t)wid * BMAX;
+  int32_t* scratch = scratch_all + (size_t)(blockIdx.x * SW + wid) * HT;
+  for (int cp = blockIdx.x * SW + wid; cp < nC; cp += gridDim.x * SW) {
+    const int c = cidx[cp];
+    const int64_t lo = ptr[c], hi = ptr[c + 1];
+    __syncwarp();
+    for (int t = lane; t < HT; t += 32) tab[t] = -1;
+    if (lane == 0) {
+      scount[wid] = 0;
+      sbcount[wid] = 0;
+      sccount[wid] = 0;
+    }
+    __syncwarp();
+    // phase 1: own coarse neighbours + F blocks of row c
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      const int32_t u = col[e];
+      if (!inF[u]) {
+        hset_insert(tab, cmap[u], &scount[wid]);
+      } else {
+        const int32_t p = partner[u];
+        bool take = true;
+        double a_cp = 0.0;
+        if (p >= 0) {
+          const int64_t ep = lookup_idx(col, lo, hi, p);
+          if (ep >= 0) a_cp = ah[ep];
+          if (ep >= 0 && p < u) take = false;
+        }
+        if (take) {
+          const int bpos = atomicAdd(&sbcount[wid], 1);
+          if (bpos < BMAX) {
+            BlkEnt bb;
+            if (p < 0) {
+              bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
+              bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
+            } else {
+              bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
+              bb.acf = (bb.f == u) ? ah[e] : a_cp;
+              bb.acg = (bb.g == u) ? ah[e] : a_cp;
+              bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
+            }
+            blk[bpos] = bb;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const int nb = sbcount[wid];
+    if (nb > BMAX) {
+      if (lane == 0) atomicExch(overflow, 1);
+      continue;
+    }
+    if (lane == 0) {  // blocks in ascending leader order (insertion sort, nb small)
+      for (int a = 1; a < nb; ++a) {
+        BlkEnt v = blk[a];
+        int q = a - 1;
+        while (q >= 0 && blk[q].lead > v.lead) {
+          blk[q + 1] = blk[q];
+          --q;
+        }
+        blk[q + 1] = v;
+      }
+    }
+    __syncwarp();
+    // phase 2: coarse neighbours of every block member
+    for (int bi = 0; bi < nb; ++bi) {
+      for (int mm = 0; mm < 2; ++mm) {
+        const int32_t u = (mm == 0) ? blk[bi].f : blk[bi].g;
+        if (u < 0) continue;
+        for (int64_t e = ptr[u] + lane; e < ptr[u + 1]; e += 32) {
+          const int32_t v = col[e];
+          if (!inF[v]) hset_insert(tab, cmap[v], &scount[wid]);
+        }
+      }
+      if (scount[wid] > (HT * 3) / 4) break;
+    }
+    __syncwarp();
+    const int nc = scount[wid];
+    if (nc > (HT * 3) / 4) {
+      if (lane == 0) atomicExch(overflow, 2);
+      continue;
+    }
+    // compact the set into scratch, then back into smem and sort
+    for (int t = lane; t < HT; t += 32) {
+      const int32_t kk = tab[t];
+      if (kk >= 0) scratch[atomicAdd(&sccount[wid], 1)] = kk;
+    }
+    __syncwarp();
+    int P = 1;
+    while (P < nc) P <<= 1;
+    for (int t = lane; t < P; t += 32) tab[t] = (t < nc) ? scratch[t] : INT32_MAX;
+    __syncwarp();
+    warp_bitonic_sort(tab, P);
+    // phase 3: values of the unique columns, ascending, chunks of 32
+    int64_t wbase = FILL ? cnt_or_ptr[cp] : 0;
+    int kept = 0;
+    for (int t0 = 0; t0 < nc; t0 += 32) {
+      const int t = t0 + lane;
+      bool keep = false;
+      int32_t c2p = INT32_MAX;
+      double sv = 0.0;
+      if (t < nc) {
+        c2p = tab[t];
+        const int32_t c2 = cidx[c2p];
+        sv = lookup(col, ah, lo, hi, c2);
+        const int64_t lo2 = ptr[c2], hi2 = ptr[c2 + 1];
+        for (int bi = 0; bi < nb; ++bi) {
+          const BlkEnt& B = blk[bi];
+          const double a2f = lookup(col, ah, lo2, hi2, B.f);
+          if (B.g < 0) {
+            if (a2f != 0.0) sv = __dsub_rn(sv, __dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)));
+          } else {
+            const double a2g = lookup(col, ah, lo2, hi2, B.g);
+            if (a2f != 0.0 || a2g != 0.0) {
+              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
+                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
+              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
+              sv = __dsub_rn(sv, __dadd_rn(t1, t2));
+            }
+          }
+        }
+        keep = (c2p == cp) || (fabs(sv) >= tau);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (FILL && keep) {
+        const int off = __popc(bal & ((1u << lane) - 1u));
+        Scol[wbase + kept + off] = c2p;
+        Sval[wbase + kept + off] = sv;
+      }
+      kept += __popc(bal);
+    }
+    if (!FILL && lane == 0) cnt_or_ptr[cp] = kept;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// dense coarse inverse: Gauss-Jordan with partial pivoting on [A | I]
+__global__ void k_dense_init(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                             const double* __restrict__ val, double* __restrict__ M) {
+  const int64_t w = 2 * (int64_t)n;
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * w; t += (int64_t)gridDim.x * TB) {
+    const int64_t i = t / w, j = t % w;
+    M[t] = (j == n + i) ? 1.0 : 0.0;
+  }
+}
+__global__ void k_dense_scatter(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                const double* __restrict__ val, double* __restrict__ M) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB)
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) M[(int64_t)i * 2 * n + col[e]] = val[e];
+}
+__global__ void k_gj_pivot(int n, int k, double* __restrict__ M, double* __restrict__ fcol,
+                           int* __restrict__ singular) {
+  // one CTA: find pivot row, swap rows k <-> p, scale row k, save the elimination column
+  __shared__ double sv[TB];
+  __shared__ int si[TB];
+  const int64_t w = 2 * (int64_t)n;
+  double best = -1.0;
+  int bi = k;
+  for (int i = k + threadIdx.x; i < n; i += TB) {
+    const double a = fabs(M[(int64_t)i * w + k]);
+    if (a > best) {
+      best = a;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = TB / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      if (sv[threadIdx.x + s] > sv[threadIdx.x] ||
+          (sv[threadIdx.x + s] == sv[threadIdx.x] && si[threadIdx.x + s] < si[threadIdx.x])) {
+        sv[threadIdx.x] = sv[threadIdx.x + s];
+        si[threadIdx.x] = si[threadIdx.x + s];
+      }
+    }
+    __syncthreads();
+  }
+  const int p = si[0];
+  if (sv[0] <= 0.0) {
+    if (threadIdx.x == 0) *singular = 1;
+    return;
+  }
+  if (p != k)
+    for (int64_t j = threadIdx.x; j < w; j += TB) {
+      const double t = M[(int64_t)k * w + j];
+      M[(int64_t)k * w + j] = M[(int64_t)p * w + j];
+      M[(int64_t)p * w + j] = t;
+    }
+  __syncthreads();
+  const double inv = 1.0 / M[(int64_t)k * w + k];
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < w; j += TB) M[(int64_t)k * w + j] *= inv;
+  for (int i = threadIdx.x; i < n; i += TB) fcol[i] = (i == k) ? 0.0 : M[(int64_t)i * w + k];
+}
+__global__ void k_gj_elim(int n, int k, double* __restrict__ M, const double* __restrict__ fcol) {
+  const int64_t w = 2 * (int64_t)n;
+  // rows i != k: M[i, :] -= f_i * M[k, :]
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * w; t += (int64_t)gridDim.x * TB) {
+    const int64_t i = t / w, j = t % w;
+    const double f = fcol[i];
+    if (f != 0.0) M[t] -= f * M[(int64_t)k * w + j];
+  }
+}
+__global__ void k_gj_extract(int n, const double* __restrict__ M, double* __restrict__ G) {
+  const int64_t w = 2 * (int64_t)n;
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * TB) {
+    const int64_t i = t / n, j = t % n;
+    G[t] = 0.5 * (M[i * w + n + j] + M[j * w + n + i]);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// application kernels
+__global__ void k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
+                            const double* __restrict__ r, const int64_t* __restrict__ Lptr,
+                            const int32_t* __restrict__ Lcol, const double* __restrict__ Lval,
+                            double* __restrict__ rn) {
+  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
+    const int c = cidx[cp];
+    double acc = D[c] * r[c];
+    for (int64_t e = Lptr[cp]; e < Lptr[cp + 1]; ++e) acc -= Lval[e] * r[Lcol[e]];
+    rn[cp] = acc;
+  }
+}
+__global__ void k_apply_bwd(int n, const int32_t* __restrict__ cmap, const double* __restrict__ D,
+                            const double* __restrict__ r, const int32_t* __restrict__ partner,
+                            const double* __restrict__ b11, const double* __restrict__ b12,
+                            const int64_t* __restrict__ LTptr, const int32_t* __restrict__ LTcol,
+                            const double* __restrict__ LTval, const double* __restrict__ zn,
+                            double* __restrict__ z) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+    const int32_t cm = cmap[i];
+    if (cm >= 0) {
+      z[i] = D[i] * zn[cm];
+    } else {
+      double acc = b11[i] * (D[i] * r[i]);
+      const int32_t p = partner[i];
+      if (p >= 0) acc += b12[i] * (D[p] * r[p]);
+      for (int64_t e = LTptr[i]; e < LTptr[i + 1]; ++e) acc -= LTval[e] * zn[LTcol[e]];
+      z[i] = D[i] * acc;
+    }
+  }
+}
+// z = G r (dense, warp per row)
+__global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __restrict__ r,
+                           double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * TB + threadIdx.x) >> 5; i < n; i += (gridDim.x * TB) >> 5) {
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc += G[(int64_t)i * n + j] * r[j];
+    acc = warp_sum(acc);
+    if (lane == 0) z[i] = acc;
+  }
+}
+
+// ============================================================================
+// host side
+static void exclusive_scan_i64(const int64_t* in, int64_t* out, int n, cudaStream_t st) {
+  size_t tmp = 0;
+  AJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
+  void* t = dalloc<char>(tmp, st);
+  AJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, st));
+  dfree(t, st);
+}
+static void exclusive_scan_i32(const int32_t* in, int32_t* out, int n, cudaStream_t st) {
+  size_t tmp = 0;
+  AJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
+  void* t = dalloc<char>(tmp, st);
+  AJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, st));
+  dfree(t, st);
+}
+template <typename T>
+static T read_scalar(const T* d, cudaStream_t st) {
+  T h;
+  AJ_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+// counts (n) -> ptr (n+1) with total; returns total
+static int64_t counts_to_ptr(int64_t* cnt, int64_t*& ptr, int n, cudaStream_t st) {
+  ptr = dalloc<int64_t>((size_t)n + 1, st);
+  if (n == 0) {
+    AJ_CUDA(cudaMemsetAsync(ptr, 0, sizeof(int64_t), st));
+    return 0;
+  }
+  exclusive_scan_i64(cnt, ptr, n, st);
+  int64_t last_c, last_p;
+  AJ_CUDA(cudaMemcpyAsync(&last_c, cnt + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  AJ_CUDA(cudaMemcpyAsync(&last_p, ptr + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  const int64_t tot = last_c + last_p;
+  AJ_CUDA(cudaMemcpyAsync(ptr + n, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  return tot;
+}
+
+void Csr::release(cudaStream_t st) {
+  dfree(ptr, st);
+  dfree(col, st);
+  dfree(val, st);
+  ptr = nullptr;
+  col = nullptr;
+  val = nullptr;
+}
+
+void Level::release(cudaStream_t st) {
+  for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)partner, (void*)b11, (void*)b12, (void*)Lptr,
+                  (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)r, (void*)z})
+    dfree(p, st);
+}
+
+// Factor one level.  Returns false on stall (nothing allocated into lv then).
+static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P, Level& lv, Csr& S,
+                         cudaStream_t st) {
+  const int n = A.n;
+  const int g = grid_for(n);
+  double* D = dalloc<double>(n, st);
+  double* ah = dalloc<double>(A.nnz, st);
+  double* dg = dalloc<double>(n, st);
+  double* lmax1 = dalloc<double>(n, st);
+  double* d1 = dalloc<double>(n, st);
+  double* q = dalloc<double>(n, st);
+  double* b11 = dalloc<double>(n, st);
+  double* b12 = dalloc<double>(n, st);
+  int32_t* prop = dalloc<int32_t>(n, st);
+  int32_t* partner = dalloc<int32_t>(n, st);
+  int32_t* leader = dalloc<int32_t>(n, st);
+  int8_t* ok1 = dalloc<int8_t>(n, st);
+  int8_t* inF = dalloc<int8_t>(n, st);
+  int8_t* nominate = dalloc<int8_t>(n, st);
+  int* counters = dalloc<int>(8, st);
+  AJ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int), st));
+  AJ_CUDA(cudaMemsetAsync(partner, 0xff, n * sizeof(int32_t), st));
+  AJ_CUDA(cudaMemsetAsync(b12, 0, n * sizeof(double), st));
+  AJ_CUDA(cudaMemsetAsync(nominate, 0, n, st));
+
+  k_rowmax_scale<<<g, TB, 0, st>>>(n, A.ptr, A.val, D);
+  AJ_LAUNCHED();
+  k_scaled_quality<<<g, TB, 0, st>>>(n, A.ptr, A.col, A.val, D, ah, dg, lmax1, d1, prop, ok1, P.kappa);
+  AJ_LAUNCHED();
+  if (latticeL == 0) {
+    k_pairs<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, dg, d1, prop, ok1, P.kappa, partner, b11, b12, q,
+                              counters + 0);
+    AJ_LAUNCHED();
+  }
+  k_blocks<<<g, TB, 0, st>>>(n, latticeL, ok1, dg, lmax1, partner, leader, q, b11, inF);
+  AJ_LAUNCHED();
+
+  int rounds = 0;
+  if (latticeL == 0) {
+    // maximal independent set of blocks on the strong graph, ranked by (q, leader)
+    uint64_t* key = dalloc<uint64_t>(n, st);
+    uint64_t* key2 = dalloc<uint64_t>(n, st);
+    int32_t* idx = dalloc<int32_t>(n, st);
+    int32_t* idx2 = dalloc<int32_t>(n, st);
+    int32_t* rank = dalloc<int32_t>(n, st);
+    int32_t* nbmin = dalloc<int32_t>(n, st);
+    int8_t* status = dalloc<int8_t>(n, st);
+    int8_t* win = dalloc<int8_t>(n, st);
+    int8_t* rem = dalloc<int8_t>(n, st);
+    AJ_CUDA(cudaMemsetAsync(status, 0, n, st));
+    AJ_CUDA(cudaMemsetAsync(win, 0, n, st));
+    AJ_CUDA(cudaMemsetAsync(rem, 0, n, st));
+    k_rank_keys<<<g, TB, 0, st>>>(n, leader, q, key, idx);
+    AJ_LAUNCHED();
+    size_t tmp = 0;
+    AJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key2, idx, idx2, n, 0, 64, st));
+    void* t = dalloc<char>(tmp, st);
+    AJ_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, key2, idx, idx2, n, 0, 64, st));
+    dfree(t, st);
+    k_rank_scatter<<<g, TB, 0, st>>>(n, idx2, rank);
+    AJ_LAUNCHED();
+    for (;;) {
+      ++rounds;
+      AJ_CUDA(cudaMemsetAsync(counters + 1, 0, sizeof(int), st));
+      k_mis_nbmin<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, rank, nbmin);
+      AJ_LAUNCHED();
+      k_mis_win<<<g, TB, 0, st>>>(n, leader, partner, status, rank, nbmin, win);
+      AJ_LAUNCHED();
+      k_mis_remove<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, win, rem);
+      AJ_LAUNCHED();
+      k_mis_apply<<<g, TB, 0, st>>>(n, leader, status, win, rem, counters + 1);
+      AJ_LAUNCHED();
+      if (read_scalar(counters + 1, st) == 0) break;
+      AJ_REQUIRE(rounds < 10000, AJ_ERR_BREAKDOWN, "independent-set rounds did not terminate");
+    }
+    k_mis_final<<<g, TB, 0, st>>>(n, leader, status, inF);
+    AJ_LAUNCHED();
+    for (void* p : {(void*)key, (void*)key2, (void*)idx, (void*)idx2, (void*)rank, (void*)nbmin,
+                    (void*)status, (void*)win, (void*)rem})
+      dfree(p, st);
+  }
+  // row-budget repair (inverse-based bound on the rows of L^{-1})
+  for (int it = 0;; ++it) {
+    AJ_CUDA(cudaMemsetAsync(counters + 2, 0, sizeof(int), st));
+    k_budget<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, P.kappa, nominate, counters + 2);
+    AJ_LAUNCHED();
+    if (read_scalar(counters + 2, st) == 0) break;
+    k_budget_apply<<<g, TB, 0, st>>>(n, partner, inF, nominate);
+    AJ_LAUNCHED();
+    AJ_CUDA(cudaMemsetAsync(nominate, 0, n, st));
+    AJ_REQUIRE(it < 100000, AJ_ERR_BREAKDOWN, "budget repair did not terminate");
+  }
+  AJ_CUDA(cudaMemsetAsync(counters + 3, 0, 2 * sizeof(int), st));
+  k_clear_nominate<<<g, TB, 0, st>>>(n, partner, inF, nominate, counters + 3, counters + 4);
+  AJ_LAUNCHED();
+  int hc[8];
+  AJ_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  const int nF = hc[3], npairsF = hc[4];
+
+  auto free_tmp = [&]() {
+    for (void* p : {(void*)ah, (void*)dg, (void*)lmax1, (void*)d1, (void*)q, (void*)prop, (void*)leader,
+                    (void*)ok1, (void*)inF, (void*)nominate, (void*)counters})
+      dfree(p, st);
+  };
+  if (nF < P.stall_frac * n || nF == 0) {
+    free_tmp();
+    for (void* p : {(void*)D, (void*)b11, (void*)b12, (void*)partner}) dfree(p, st);
+    return false;
+  }
+  const int nC = n - nF;
+  lv.n = n;
+  lv.nF = nF;
+  lv.nC = nC;
+  lv.npairs = npairsF;
+  lv.rounds = rounds;
+  lv.D = D;
+  lv.b11 = b11;
+  lv.b12 = b12;
+  lv.cmap = dalloc<int32_t>(n, st);
+  lv.cidx = dalloc<int32_t>(std::max(nC, 1), st);
+  lv.partner = dalloc<int32_t>(n, st);
+  {
+    int32_t* flag = dalloc<int32_t>(n, st);
+    int32_t* scan = dalloc<int32_t>(n, st);
+    k_cflags<<<g, TB, 0, st>>>(n, inF, flag);
+    AJ_LAUNCHED();
+    exclusive_scan_i32(flag, scan, n, st);
+    // b11/b12 of C nodes zeroed inside k_cmap (they were block data of non-F nodes)
+    k_cmap<<<g, TB, 0, st>>>(n, inF, scan, lv.cmap, lv.cidx, lv.partner, partner, b11, b12);
+    AJ_LAUNCHED();
+    dfree(flag, st);
+    dfree(scan, st);
+  }
+  // L (forward) rows over coarse nodes
+  {
+    int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
+    const int gc = grid_for(nC);
+    k_L_rows<false><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
+                                        P.tau_drop, cnt, nullptr, nullptr);
+    AJ_LAUNCHED();
+    lv.nnzL = counts_to_ptr(cnt, lv.Lptr, nC, st);
+    lv.Lcol = dalloc<int32_t>(lv.nnzL, st);
+    lv.Lval = dalloc<double>(lv.nnzL, st);
+    k_L_rows<true><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
+                                       P.tau_drop, lv.Lptr, lv.Lcol, lv.Lval);
+    AJ_LAUNCHED();
+    dfree(cnt, st);
+  }
+  // L^T (backward) rows over level nodes
+  {
+    int64_t* cnt = dalloc<int64_t>(n, st);
+    k_LT_rows<false><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap, P.tau_drop,
+                                        cnt, nullptr, nullptr);
+    AJ_LAUNCHED();
+    lv.nnzLT = counts_to_ptr(cnt, lv.LTptr, n, st);
+    lv.LTcol = dalloc<int32_t>(lv.nnzLT, st);
+    lv.LTval = dalloc<double>(lv.nnzLT, st);
+    k_LT_rows<true><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap, P.tau_drop,
+                                       lv.LTptr, lv.LTcol, lv.LTval);
+    AJ_LAUNCHED();
+    dfree(cnt, st);
+  }
+  // Schur complement on the coarse nodes
+  {
+    S.n = nC;
+    int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
+    const int nwarps_total = std::min(ceil_div(std::max(nC, 1), 1), num_sms() * 16 * SW);
+    const int gs = std::max(1, ceil_div(nwarps_total, SW));
+    int32_t* cand = dalloc<int32_t>((size_t)gs * SW * HT, st);
+    static bool attr_set = false;
+    if (!attr_set) {
+      AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      attr_set = true;
+    }
+    int* ovf = counters + 5;
+    AJ_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
+                                                     b12, P.tau_drop, cand, cnt, nullptr, nullptr, ovf);
+    AJ_LAUNCHED();
+    const int o = read_scalar(ovf, st);
+    AJ_REQUIRE(o == 0, AJ_ERR_CAPACITY,
+               o == 1 ? "Schur complement: more than 96 pivot blocks adjacent to one row (raise tau_drop)"
+                      : "Schur complement: more than 3072 candidate columns in one row (raise tau_drop)");
+    S.nnz = counts_to_ptr(cnt, S.ptr, nC, st);
+    S.col = dalloc<int32_t>(S.nnz, st);
+    S.val = dalloc<double>(S.nnz, st);
+    k_schur<true><<<gs, SW * 32, kSchurSmem, st>>>(nC, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
+                                                    b12, P.tau_drop, cand, S.ptr, S.col, S.val, ovf);
+    AJ_LAUNCHED();
+    dfree(cand, st);
+    dfree(cnt, st);
+    lv.nnzS = S.nnz;
+  }
+  dfree(partner, st);
+  free_tmp();
+  return true;
+}
+
+Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,
+                        cudaStream_t st) {
+  AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "precond_setup: L must be >= 3");
+  AJ_REQUIRE(P.kappa > 1.0 && P.tau_drop >= 0.0 && P.tau_strong >= 0.0 && P.cand_cap >= 64,
+             AJ_ERR_ARG, "precond_setup: invalid parameters");
+  const int64_t n64 = (int64_t)L * L * L;
+  AJ_REQUIRE(n64 < (int64_t)INT32_MAX, AJ_ERR_ARG, "precond_setup: L^3 exceeds int32 indexing");
+  cudaEvent_t e0, e1;
+  AJ_CUDA(cudaEventCreate(&e0));
+  AJ_CUDA(cudaEventCreate(&e1));
+  AJ_CUDA(cudaEventRecord(e0, st));
+  ProfScope ps(PROF_SETUP, 0.0, st);
+  Precond* K = new Precond();
+  K->L = L;
+  K->n0 = (int)n64;
+  K->P = P;
+  try {
+    Csr A;
+    A.n = (int)n64;
+    A.nnz = 7 * n64;
+    A.ptr = dalloc<int64_t>(n64 + 1, st);
+    A.col = dalloc<int32_t>(A.nnz, st);
+    A.val = dalloc<double>(A.nnz, st);
+    k_lattice_csr<<<std::min(grid_for(n64), num_sms() * 16), TB, 0, st>>>(L, eps, hop, sigma, A.ptr, A.col,
+                                                                           A.val);
+    AJ_LAUNCHED();
+    for (int lev = 0; lev < P.max_levels && lev < 256; ++lev) {
+      if (A.n <= P.n_coarse_max) break;
+      Level lv;
+      Csr S;
+      if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
+      if (lev > 0) {
+        lv.r = dalloc<double>(lv.n, st);
+        lv.z = dalloc<double>(lv.n, st);
+      }
+      K->lv.push_back(lv);
+      A.release(st);
+      A = S;
+    }
+    AJ_REQUIRE(A.n <= P.dense_cap, AJ_ERR_BREAKDOWN,
+               "multilevel ILDL breakdown: coarse system of size " + std::to_string(A.n) +
+                   " exceeds dense_cap (increase kappa)");
+    const int nc = A.n;
+    K->nc = nc;
+    K->rc = dalloc<double>(std::max(nc, 1), st);
+    K->zc = dalloc<double>(std::max(nc, 1), st);
+    K->G = dalloc<double>(std::max<int64_t>((int64_t)nc * nc, 1), st);
+    if (nc > 0) {
+      double* M = dalloc<double>((int64_t)nc * 2 * nc, st);
+      double* fcol = dalloc<double>(nc, st);
+      int* sing = dalloc<int>(1, st);
+      AJ_CUDA(cudaMemsetAsync(sing, 0, sizeof(int), st));
+      const int gd = std::min(grid_for((int64_t)nc * 2 * nc), num_sms() * 16);
+      k_dense_init<<<gd, TB, 0, st>>>(nc, A.ptr, A.col, A.val, M);
+      AJ_LAUNCHED();
+      k_dense_scatter<<<grid_for(nc), TB, 0, st>>>(nc, A.ptr, A.col, A.val, M);
+      AJ_LAUNCHED();
+      for (int k = 0; k < nc; ++k) {
+        k_gj_pivot<<<1, TB, 0, st>>>(nc, k, M, fcol, sing);
+        AJ_LAUNCHED();
+        k_gj_elim<<<gd, TB, 0, st>>>(nc, k, M, fcol);
+        AJ_LAUNCHED();
+      }
+      AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
+      k_gj_extract<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, K->G);
+      AJ_LAUNCHED();
+      dfree(M, st);
+      dfree(fcol, st);
+      dfree(sing, st);
+    }
+    A.release(st);
+  } catch (...) {
+    precond_destroy(K, st);
+    throw;
+  }
+  AJ_CUDA(cudaEventRecord(e1, st));
+  AJ_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  // info
+  aj_precond_info& I = K->info;
+  memset(&I, 0, sizeof(I));
+  I.levels = (int)K->lv.size();
+  I.coarse_n = K->nc;
+  I.nnz_A = 7 * n64;
+  for (size_t l = 0; l < K->lv.size(); ++l) {
+    const Level& v = K->lv[l];
+    I.nnz_L += v.nnzL;
+    I.level_n[l] = v.n;
+    I.level_nF[l] = v.nF;
+    I.level_pairs[l] = v.npairs;
+    I.level_nnzS[l] = v.nnzS;
+  }
+  I.setup_ms = ms;
+  K->bytes_per_apply = precond_bytes_per_apply(K);
+  return K;
+}
+
+void precond_destroy(Precond* K, cudaStream_t st) {
+  if (!K) return;
+  for (auto& l : K->lv) l.release(st);
+  dfree(K->G, st);
+  dfree(K->rc, st);
+  dfree(K->zc, st);
+  delete K;
+}
+
+// z = K^{-1} r
+void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st) {
+  ProfScope ps(PROF_PREC, (double)K->bytes_per_apply, st);
+  const int nl = (int)K->lv.size();
+  // forward sweep
+  const double* rin = r;
+  for (int l = 0; l < nl; ++l) {
+    const Level& v = K->lv[l];
+    double* rn = (l + 1 < nl) ? K->lv[l + 1].r : K->rc;
+    if (v.nC > 0) {
+      k_apply_fwd<<<grid_for(v.nC), TB, 0, st>>>(v.nC, v.cidx, v.D, rin, v.Lptr, v.Lcol, v.Lval, rn);
+      AJ_LAUNCHED();
+    }
+    rin = rn;
+  }
+  // coarse
+  if (K->nc > 0) {
+    double* zc = (nl == 0) ? z : K->zc;
+    k_dense_mv<<<std::max(1, ceil_div((int64_t)K->nc * 32, TB)), TB, 0, st>>>(K->nc, K->G, rin, zc);
+    AJ_LAUNCHED();
+  }
+  // backward sweep
+  for (int l = nl - 1; l >= 0; --l) {
+    const Level& v = K->lv[l];
+    const double* rl = (l == 0) ? r : v.r;
+    double* zl = (l == 0) ? z : v.z;
+    const double* zn = (l + 1 < nl) ? K->lv[l + 1].z : K->zc;
+    k_apply_bwd<<<grid_for(v.n), TB, 0, st>>>(v.n, v.cmap, v.D, rl, v.partner, v.b11, v.b12, v.LTptr, v.LTcol,
+                                              v.LTval, zn, zl);
+    AJ_LAUNCHED();
+  }
+}
+
+int64_t precond_bytes_per_apply(const Precond* K) {
+  // algorithmic HBM bytes of one application: every stored factor entry read once
+  // (8 B value + 4 B index) plus per-level vectors (r read twice, D, z/rn writes)
+  int64_t b = 0;
+  for (const auto& v : K->lv) {
+    b += (v.nnzL + v.nnzLT) * 12;
+    b += (int64_t)v.n * (8 /*D*/ + 8 /*r*/ + 8 /*z*/ + 4 /*cmap*/ + 8 * 2 /*b11,b12 for F*/ + 4 /*partner*/);
+    b += (int64_t)v.nC * (4 + 8 + 8 + 8);  // cidx, D_c r_c, rn write, L ptr
+  }
+  b += (int64_t)K->nc * K->nc * 8;
+  return b;
+}
+
+}  // namespace aj

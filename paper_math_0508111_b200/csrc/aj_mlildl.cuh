@@ -1,0 +1,56 @@
+// Multilevel ILDL data structures (see aj_mlildl.cu).
+#pragma once
+#include <vector>
+
+#include "aj_common.cuh"
+
+namespace aj {
+
+struct Csr {
+  int n = 0;
+  int64_t nnz = 0;
+  int64_t* ptr = nullptr;  // n+1
+  int32_t* col = nullptr;  // nnz, sorted per row
+  double* val = nullptr;   // nnz
+  void release(cudaStream_t st);
+};
+
+struct Level {
+  int n = 0, nF = 0, nC = 0, npairs = 0, rounds = 0;
+  int64_t nnzL = 0, nnzLT = 0, nnzS = 0;
+  double* D = nullptr;          // n   symmetric scaling of this level
+  int32_t* cmap = nullptr;      // n   coarse index of C nodes, -1 for F
+  int32_t* cidx = nullptr;      // nC  level index of coarse node c'
+  int32_t* partner = nullptr;   // n   2x2 partner of F nodes, else -1
+  double* b11 = nullptr;        // n   B^{-1}[f,f]   (F nodes)
+  double* b12 = nullptr;        // n   B^{-1}[f,g]   (F nodes of a pair)
+  int64_t* Lptr = nullptr;      // nC+1
+  int32_t* Lcol = nullptr;      // level index of F node
+  double* Lval = nullptr;       // L_cf * D_f
+  int64_t* LTptr = nullptr;     // n+1 (F rows only non-empty)
+  int32_t* LTcol = nullptr;     // coarse index
+  double* LTval = nullptr;      // L_cf
+  double* r = nullptr;          // level workspace (levels >= 1)
+  double* z = nullptr;
+  void release(cudaStream_t st);
+};
+
+struct Precond {
+  int L = 0, n0 = 0;
+  aj_precond_params P{};
+  std::vector<Level> lv;
+  int nc = 0;
+  double* G = nullptr;   // nc x nc dense symmetric inverse of the coarse Schur complement
+  double* rc = nullptr;
+  double* zc = nullptr;
+  aj_precond_info info{};
+  int64_t bytes_per_apply = 0;
+};
+
+Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,
+                        cudaStream_t st);
+void precond_destroy(Precond* K, cudaStream_t st);
+void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st);
+int64_t precond_bytes_per_apply(const Precond* K);
+
+}  // namespace aj

@@ -1,0 +1,425 @@
+// Correction-equation SQMR and the symmetric Jacobi-Davidson driver.
+//
+// PAPER.md sect. 4.2 (l.380-421): JD expands V with corrections from
+//   (I - Q~Q~^T)(A - theta I)(I - Q~Q~^T) z = -r,   Q~ = [Q, u],
+// solved approximately by the simplified QMR method (l.412-416, l.986) with the
+// projected preconditioner (I - Y H^{-1} Q~^T) K^{-1}, Y = K^{-1} Q~, H = Q~^T Y
+// -- the block form of (I - u w^T / w^T u) K^{-1}, K w = u (l.414-415).
+// K is the multilevel ILDL of A - sigma I (aj_mlildl.cu), built once per solve.
+//
+// Device residency: every SQMR scalar (rho, tau, theta, alpha, ...) lives in
+// device memory and is updated by the "last block" of the fused reduction
+// kernels, so one SQMR step is: fused stencil+dots, two fused update kernels,
+// the preconditioner sweep, two tall-skinny dot kernels and one update kernel;
+// the host only reads the residual norm for the stopping test.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "aj_common.cuh"
+#include "aj_kernels.cuh"
+#include "aj_mlildl.cuh"
+#include "aj_solver.cuh"
+
+namespace aj {
+
+constexpr int TB = 256;
+static int sgrid(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, TB), (int64_t)num_sms() * 8));
+}
+
+// scalar slots
+enum { S_TAU = 0, S_THETA, S_A1, S_A2, S_RX2, S_BRK, S_RHO0, S_RHO1, S_NB, S_COUNT = 16 };
+
+// t' = t - Qt c ;  alpha = rho/sigma_q ; r -= alpha t' ; ||r||^2 -> theta, tau, coefficients
+__global__ void __launch_bounds__(TB)
+    k_sqmr_B(int64_t n, int m, const double* __restrict__ Qt, double* __restrict__ t, double* __restrict__ r,
+             const double* __restrict__ dotsA, const double* __restrict__ rho_cur, double* __restrict__ sc,
+             RedBuf rb) {
+  __shared__ double sc_c[32];
+  if (threadIdx.x < m) sc_c[threadIdx.x] = dotsA[threadIdx.x];
+  __syncthreads();
+  const double sig = dotsA[m];
+  const double alpha = (*rho_cur) / sig;
+  double acc[1] = {0.0};
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    double tv = t[s];
+    for (int c = 0; c < m; ++c) tv -= __ldg(&Qt[(int64_t)c * n + s]) * sc_c[c];
+    t[s] = tv;
+    const double rv = r[s] - alpha * tv;
+    r[s] = rv;
+    acc[0] += rv * rv;
+  }
+  if (block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x) && threadIdx.x == 0) {
+    const double rr = rb.out[0];
+    const double tau = sc[S_TAU], th_old = sc[S_THETA];
+    const double th = sqrt(rr) / tau;
+    const double c2 = 1.0 / (1.0 + th * th);
+    sc[S_A1] = c2 * th_old * th_old;
+    sc[S_A2] = c2 * alpha;
+    sc[S_THETA] = th;
+    sc[S_TAU] = tau * th * sqrt(c2);
+    if (sig == 0.0 || !isfinite(alpha)) sc[S_BRK] = 1.0;
+  }
+}
+
+// d = a1 d + a2 q ; x += d ; s = a1 s + a2 t' ; rx -= s ; ||rx||^2
+__global__ void __launch_bounds__(TB)
+    k_sqmr_C(int64_t n, const double* __restrict__ q, const double* __restrict__ t, double* __restrict__ d,
+             double* __restrict__ x, double* __restrict__ sv, double* __restrict__ rx, double* __restrict__ sc,
+             RedBuf rb) {
+  const double a1 = sc[S_A1], a2 = sc[S_A2];
+  double acc[1] = {0.0};
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    const double dv = a1 * d[s] + a2 * q[s];
+    d[s] = dv;
+    x[s] += dv;
+    const double svv = a1 * sv[s] + a2 * t[s];
+    sv[s] = svv;
+    const double rxv = rx[s] - svv;
+    rx[s] = rxv;
+    acc[0] += rxv * rxv;
+  }
+  if (block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x) && threadIdx.x == 0) sc[S_RX2] = rb.out[0];
+}
+
+// g = Hinv (Q~^T w); rho_new = w^T r - (Y^T r) . g; q = (w - Y g) + beta q
+__global__ void __launch_bounds__(TB)
+    k_sqmr_F(int64_t n, int m, const double* __restrict__ Y, const double* __restrict__ w,
+             double* __restrict__ q, const double* __restrict__ dQw, const double* __restrict__ dYr,
+             const double* __restrict__ Hinv, const double* __restrict__ rho_prev, double* __restrict__ rho_out,
+             int first, double* __restrict__ sc) {
+  __shared__ double g[32];
+  __shared__ double s_beta;
+  if (threadIdx.x < m) {
+    double a = 0.0;
+    for (int b = 0; b < m; ++b) a += Hinv[threadIdx.x + b * m] * dQw[b];
+    g[threadIdx.x] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rho = dYr[m];
+    for (int c = 0; c < m; ++c) rho -= dYr[c] * g[c];
+    const double beta = first ? 0.0 : rho / (*rho_prev);
+    s_beta = beta;
+    if (blockIdx.x == 0) {
+      *rho_out = rho;
+      if (rho == 0.0 || !isfinite(beta)) sc[S_BRK] = 1.0;
+    }
+  }
+  __syncthreads();
+  const double beta = s_beta;
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    double u = w[s];
+    for (int c = 0; c < m; ++c) u -= __ldg(&Y[(int64_t)c * n + s]) * g[c];
+    q[s] = u + (first ? 0.0 : beta * q[s]);
+  }
+}
+
+__global__ void k_sqmr_init_scalars(double* sc, const double* nb2) {
+  const double nb = sqrt(*nb2);
+  for (int i = 0; i < S_COUNT; ++i) sc[i] = 0.0;
+  sc[S_TAU] = nb;
+  sc[S_NB] = nb;
+  sc[S_RX2] = *nb2;
+  sc[S_RHO0] = 1.0;
+  sc[S_RHO1] = 1.0;
+}
+
+// ----------------------------------------------------------------------------
+// small dense kernels (one CTA): symmetric eigen (parallel cyclic Jacobi,
+// round-robin pairing), sorted by |theta| then theta; H^{-1} by Gauss-Jordan.
+constexpr int EIG_MAX = 48;
+__global__ void __launch_bounds__(256) k_small_eig(int j, int ldm, const double* __restrict__ Min,
+                                                   double* __restrict__ theta, double* __restrict__ S) {
+  __shared__ double A[EIG_MAX][EIG_MAX + 1];
+  __shared__ double Vv[EIG_MAX][EIG_MAX + 1];
+  __shared__ double cs[EIG_MAX / 2], sn[EIG_MAX / 2];
+  __shared__ int pp[EIG_MAX / 2], qq[EIG_MAX / 2];
+  __shared__ double s_off, s_tot;
+  __shared__ int order[EIG_MAX];
+  const int tid = threadIdx.x;
+  for (int t = tid; t < j * j; t += blockDim.x) {
+    const int a = t % j, b = t / j;
+    A[a][b] = 0.5 * (Min[a + b * ldm] + Min[b + a * ldm]);
+    Vv[a][b] = (a == b) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int J2 = (j + 1) & ~1;  // even number of players (dummy = j if odd)
+  const int npair = J2 / 2;
+  for (int sweep = 0; sweep < 40 && j > 1; ++sweep) {
+    if (tid == 0) {
+      double off = 0.0, tot = 0.0;
+      for (int a = 0; a < j; ++a)
+        for (int b = 0; b < j; ++b) {
+          const double v = A[a][b] * A[a][b];
+          tot += v;
+          if (a != b) off += v;
+        }
+      s_off = off;
+      s_tot = tot;
+    }
+    __syncthreads();
+    if (s_off <= 1e-32 * s_tot || s_off == 0.0) break;
+    for (int rd = 0; rd < J2 - 1; ++rd) {
+      if (tid < npair) {
+        int p, q;
+        if (tid == 0) {
+          p = rd;
+          q = J2 - 1;
+        } else {
+          p = (rd + tid) % (J2 - 1);
+          q = (rd - tid + (J2 - 1)) % (J2 - 1);
+        }
+        if (p > q) {
+          const int tmp = p;
+          p = q;
+          q = tmp;
+        }
+        double c = 1.0, s = 0.0;
+        if (q < j) {
+          const double apq = A[p][q];
+          if (apq != 0.0) {
+            const double tau = (A[q][q] - A[p][p]) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        }
+        pp[tid] = p;
+        qq[tid] = q;
+        cs[tid] = c;
+        sn[tid] = s;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int t = tid; t < npair * j; t += blockDim.x) {
+        const int pi = t / j, k = t % j;
+        const int p = pp[pi], q = qq[pi];
+        if (q >= j) continue;
+        const double c = cs[pi], s = sn[pi];
+        const double ap = A[p][k], aq = A[q][k];
+        A[p][k] = c * ap - s * aq;
+        A[q][k] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A J ; V <- V J
+      for (int t = tid; t < npair * j; t += blockDim.x) {
+        const int pi = t / j, k = t % j;
+        const int p = pp[pi], q = qq[pi];
+        if (q >= j) continue;
+        const double c = cs[pi], s = sn[pi];
+        const double ap = A[k][p], aq = A[k][q];
+        A[k][p] = c * ap - s * aq;
+        A[k][q] = s * ap + c * aq;
+        const double vp = Vv[k][p], vq = Vv[k][q];
+        Vv[k][p] = c * vp - s * vq;
+        Vv[k][q] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    for (int a = 0; a < j; ++a) order[a] = a;
+    for (int a = 1; a < j; ++a) {  // sort by (|theta|, theta)
+      const int v = order[a];
+      const double tv = A[v][v];
+      int b = a - 1;
+      while (b >= 0) {
+        const double tb = A[order[b]][order[b]];
+        const bool greater = (fabs(tb) > fabs(tv)) || (fabs(tb) == fabs(tv) && tb > tv);
+        if (!greater) break;
+        order[b + 1] = order[b];
+        --b;
+      }
+      order[b + 1] = v;
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < j * j; t += blockDim.x) {
+    const int a = t % j, b = t / j;
+    S[a + b * j] = Vv[a][order[b]];
+  }
+  for (int t = tid; t < j; t += blockDim.x) theta[t] = A[order[t]][order[t]];
+}
+
+__global__ void k_small_inv(int m, const double* __restrict__ H, double* __restrict__ Hinv, double* sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double A[17][34];
+  for (int a = 0; a < m; ++a)
+    for (int b = 0; b < 2 * m; ++b) A[a][b] = (b < m) ? 0.5 * (H[a + b * m] + H[b + a * m]) : (b - m == a ? 1.0 : 0.0);
+  for (int k = 0; k < m; ++k) {
+    int p = k;
+    for (int a = k + 1; a < m; ++a)
+      if (fabs(A[a][k]) > fabs(A[p][k])) p = a;
+    if (A[p][k] == 0.0) {
+      sc[S_BRK] = 2.0;
+      return;
+    }
+    if (p != k)
+      for (int b = 0; b < 2 * m; ++b) {
+        const double t = A[k][b];
+        A[k][b] = A[p][b];
+        A[p][b] = t;
+      }
+    const double inv = 1.0 / A[k][k];
+    for (int b = 0; b < 2 * m; ++b) A[k][b] *= inv;
+    for (int a = 0; a < m; ++a)
+      if (a != k) {
+        const double f = A[a][k];
+        if (f != 0.0)
+          for (int b = 0; b < 2 * m; ++b) A[a][b] -= f * A[k][b];
+      }
+  }
+  for (int a = 0; a < m; ++a)
+    for (int b = 0; b < m; ++b) Hinv[a + b * m] = A[a][m + b];
+}
+
+// M[:, j] and M[j, :] <- dots (j+1 values)
+__global__ void k_set_mcol(double* M, int ldm, int j, const double* __restrict__ dots) {
+  const int a = threadIdx.x;
+  if (a <= j) {
+    M[a + j * ldm] = dots[a];
+    M[j + a * ldm] = dots[a];
+  }
+}
+// M <- diag(theta[off .. off+cnt))
+__global__ void k_set_mdiag(double* M, int ldm, int cnt, const double* __restrict__ theta, int off) {
+  for (int t = threadIdx.x; t < cnt * cnt; t += blockDim.x) {
+    const int a = t % cnt, b = t / cnt;
+    M[a + b * ldm] = (a == b) ? theta[off + a] : 0.0;
+  }
+}
+// y = a*x + b*y with (a, b) = (1, -theta[0]) style device scalar: r = Au - theta u
+__global__ void k_resid(int64_t n, const double* __restrict__ Au, const double* __restrict__ u,
+                        const double* __restrict__ theta, double* __restrict__ r, RedBuf rb) {
+  const double th = theta[0];
+  double acc[1] = {0.0};
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    const double v = Au[s] - th * u[s];
+    r[s] = v;
+    acc[0] += v * v;
+  }
+  block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x);
+}
+// start vector: uniform(-0.5, 0.5) from the counter stream `key`
+__global__ void k_start(int64_t n, uint64_t key, double* __restrict__ v) {
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB)
+    v[s] = uniform01(key, (uint64_t)s) - 0.5;
+}
+// max |eps|
+__global__ void k_absmax(int64_t n, const double* __restrict__ x, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB)
+    m = fmax(m, fabs(x[s]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+__global__ void k_negate_proj(int64_t n, double* __restrict__ b, const double* __restrict__ r,
+                              const double* __restrict__ Qt, int m, const double* __restrict__ c) {
+  __shared__ double sc_c[32];
+  if (threadIdx.x < m) sc_c[threadIdx.x] = c[threadIdx.x];
+  __syncthreads();
+  for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
+    double v = r[s];
+    for (int a = 0; a < m; ++a) v -= __ldg(&Qt[(int64_t)a * n + s]) * sc_c[a];
+    b[s] = -v;
+  }
+}
+
+// ============================================================================
+Workspace::Workspace(int64_t n_, cudaStream_t st) : n(n_) {
+  rs.init(st);
+  sc = dalloc<double>(S_COUNT, st);
+  small = dalloc<double>(8192, st);
+  for (int i = 0; i < 9; ++i) vec[i] = dalloc<double>(n, st);
+}
+void Workspace::release(cudaStream_t st) {
+  rs.release(st);
+  dfree(sc, st);
+  dfree(small, st);
+  for (int i = 0; i < 9; ++i) dfree(vec[i], st);
+}
+
+// SQMR on the projected operator.  Qt/Y: n x (m+1); column m of Qt holds q, column m of Y holds w.
+// b: right-hand side (already orthogonal to Q~); x: solution out.
+SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, double shift, const double* Qt,
+                    const double* Y, int m, const double* Hinv, const double* b, double* x, double tol,
+                    int maxit, Workspace& ws, cudaStream_t st) {
+  const int64_t n = ws.n;
+  double* Qtm = const_cast<double*>(Qt);
+  double* Ym = const_cast<double*>(Y);
+  double* q = Qtm + (int64_t)m * n;
+  double* w = Ym + (int64_t)m * n;
+  double *r = ws.vec[0], *t = ws.vec[1], *d = ws.vec[2], *sv = ws.vec[3], *rx = ws.vec[4];
+  double* sc = ws.sc;
+  double* dA = ws.small;          // m+1  (padded 32)
+  double* dQw = ws.small + 64;    // m    (padded)
+  double* dYr = ws.small + 128;   // m+1  (padded)
+  double* nb2 = ws.small + 192;   // 1
+  double* red = ws.small + 200;   // scratch outs
+  SqmrResult res;
+  launch_copy(r, b, n, st);
+  launch_copy(rx, b, n, st);
+  launch_fill(x, 0.0, n, st);
+  launch_fill(d, 0.0, n, st);
+  launch_fill(sv, 0.0, n, st);
+  launch_dot(nb2, b, b, n, ws.rs, st);
+  k_sqmr_init_scalars<<<1, 1, 0, st>>>(sc, nb2);
+  AJ_LAUNCHED();
+  double hs[S_COUNT];
+  AJ_CUDA(cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  const double nb = hs[S_NB];
+  if (nb == 0.0) {
+    res.iters = 0;
+    res.relres = 0.0;
+    return res;
+  }
+  const double sig_total = shift;  // operator A - (sigma + shift) I; caller folds sigma in
+  auto precond_proj = [&](int step) {
+    // w = K^{-1} r ; q = (w - Y Hinv Q~^T w) + beta q ; rho
+    if (K)
+      precond_run(K, w, r, st);
+    else
+      launch_copy(w, r, n, st);
+    if (m > 0) launch_multi_dot(dQw, Qt, m, n, w, n, ws.rs, st);
+    launch_multi_dot(dYr, Y, m + 1, n, r, n, ws.rs, st);
+    double* rho_out = sc + ((step & 1) ? S_RHO1 : S_RHO0);
+    const double* rho_prev = sc + ((step & 1) ? S_RHO0 : S_RHO1);
+    ProfScope ps(PROF_SQMR, 8.0 * n * (m + 3), st);
+    k_sqmr_F<<<sgrid(n), TB, 0, st>>>(n, m, Y, w, q, dQw, dYr, Hinv, rho_prev, rho_out, step == 0 ? 1 : 0, sc);
+    AJ_LAUNCHED();
+  };
+  precond_proj(0);
+  int it = 0;
+  double relres = 1.0;
+  for (it = 1; it <= maxit; ++it) {
+    // t = (A - sig I) q with fused [Q~ | q]^T t
+    launch_spmv_dots(t, q, eps, L, hop, sig_total, Qt, n, m + 1, ws.rs.buf(dA, 0), st);
+    const double* rho_cur = sc + (((it - 1) & 1) ? S_RHO1 : S_RHO0);
+    {
+      ProfScope ps(PROF_SQMR, 8.0 * n * (m + 4 + 10), st);
+      k_sqmr_B<<<sgrid(n), TB, 0, st>>>(n, m, Qt, t, r, dA, rho_cur, sc, ws.rs.buf(red, 1));
+      AJ_LAUNCHED();
+      k_sqmr_C<<<sgrid(n), TB, 0, st>>>(n, q, t, d, x, sv, rx, sc, ws.rs.buf(red + 8, 2));
+      AJ_LAUNCHED();
+    }
+    AJ_CUDA(cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    AJ_CUDA(cudaStreamSynchronize(st));
+    relres = sqrt(hs[S_RX2]) / nb;
+    if (hs[S_BRK] != 0.0) {
+      res.breakdown = true;
+      break;
+    }
+    if (relres <= tol || it == maxit) break;
+    precond_proj(it);
+  }
+  res.iters = std::min(it, maxit);
+  res.relres = relres;
+  return res;
+}
+
+}  // namespace aj

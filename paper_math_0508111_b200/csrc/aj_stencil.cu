@@ -1,0 +1,120 @@
+// Anderson lattice: disorder generation and the matrix-free fp64 stencil SpMV.
+//
+// PAPER.md sect. 3, Eq. (eigenequation) l.182-186 and l.282-285 ("the
+// underlying matrix-vector multiplication ... only the diagonal needs to be
+// stored").  HBM-bound: 24 algorithmic bytes per site (read eps, x; write y).
+//
+// Kernel design (DESIGN.md sect. 4.1): a 2.5-D sweep.  A CTA owns a
+// 32 (x) by 8 (y) column tile and marches along z over a chunk of planes,
+// keeping x(k-1), x(k), x(k+1) of its own column in registers; the four
+// in-plane neighbours are re-read through L1 (they are the neighbouring
+// lanes'/warps' loads of the same plane), so every x element leaves HBM once.
+#include "aj_common.cuh"
+#include "aj_kernels.cuh"
+
+namespace aj {
+
+__global__ void k_disorder(double* __restrict__ eps, int64_t n, double W, uint64_t seed) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double u = uniform01(seed, (uint64_t)s);
+    eps[s] = (u - 0.5) * W;  // one subtraction (exact) then one multiply: bit-exact
+  }
+}
+
+void launch_disorder(double* eps, int L, double W, uint64_t seed, cudaStream_t st) {
+  int64_t n = (int64_t)L * L * L;
+  int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 16);
+  k_disorder<<<grid, 256, 0, st>>>(eps, n, W, seed);
+  AJ_LAUNCHED();
+}
+
+constexpr int SBX = 32, SBY = 8;
+
+// y = (A - sig I) x; optional fused dot products  dots[c] += sum_s y_s * W_c[s]
+// for the NV vectors W_c = Wv + c*ld (column block), reduced with the
+// last-block epilogue into rb.out[0..NV).
+template <int NV>
+__global__ void __launch_bounds__(SBX* SBY)
+    k_spmv(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps,
+           int L, double hop, double sig, int kchunk, const double* __restrict__ Wv, int64_t ld,
+           RedBuf rb) {
+  const int i = blockIdx.x * SBX + threadIdx.x;
+  const int j = blockIdx.y * SBY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, L);
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+  if (i < L && j < L && k0 < L) {
+    const int64_t P = (int64_t)L * L;
+    const int im = (i == 0) ? L - 1 : i - 1, ip = (i == L - 1) ? 0 : i + 1;
+    const int jm = (j == 0) ? L - 1 : j - 1, jp = (j == L - 1) ? 0 : j + 1;
+    const int64_t r0 = (int64_t)j * L, rm = (int64_t)jm * L, rp = (int64_t)jp * L;
+    const int km = (k0 == 0) ? L - 1 : k0 - 1;
+    double xm = __ldg(&x[km * P + r0 + i]);
+    double xc = __ldg(&x[k0 * P + r0 + i]);
+    for (int k = k0; k < k1; ++k) {
+      const int kp = (k == L - 1) ? 0 : k + 1;
+      const double xp = __ldg(&x[kp * P + r0 + i]);
+      const int64_t b = k * P;
+      const double s = (__ldg(&x[b + r0 + im]) + __ldg(&x[b + r0 + ip])) +
+                       (__ldg(&x[b + rm + i]) + __ldg(&x[b + rp + i])) + (xm + xp);
+      const double v = hop * s + (__ldg(&eps[b + r0 + i]) - sig) * xc;
+      y[b + r0 + i] = v;
+      if constexpr (NV > 0) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] += v * __ldg(&Wv[c * ld + b + r0 + i]);
+      }
+      xm = xc;
+      xc = xp;
+    }
+  }
+  if constexpr (NV > 0) block_reduce_finalize<NV, SBX * SBY>(acc, rb, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                                                       gridDim.x * gridDim.y * gridDim.z);
+}
+
+static dim3 spmv_grid(int L, int& kchunk) {
+  int tiles = ceil_div(L, SBX) * ceil_div(L, SBY);
+  // aim for >= 4 waves of 256-thread CTAs over 148 SMs, chunks of >= 4 planes
+  int want = num_sms() * 8;
+  int nz = std::max(1, std::min(L, ceil_div(want, tiles)));
+  kchunk = std::max(4, ceil_div(L, nz));
+  kchunk = std::min(kchunk, L);
+  nz = ceil_div(L, kchunk);
+  return dim3(ceil_div(L, SBX), ceil_div(L, SBY), nz);
+}
+
+int spmv_grid_blocks(int L) {
+  int kc;
+  dim3 g = spmv_grid(L, kc);
+  return (int)(g.x * g.y * g.z);
+}
+
+void launch_spmv(double* y, const double* x, const double* eps, int L, double hop, double sig,
+                 cudaStream_t st) {
+  int kc;
+  dim3 g = spmv_grid(L, kc);
+  ProfScope ps(PROF_SPMV, 24.0 * L * L * L, st);
+  k_spmv<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
+  AJ_LAUNCHED();
+}
+
+void launch_spmv_dots(double* y, const double* x, const double* eps, int L, double hop, double sig,
+                      const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st) {
+  int kc;
+  dim3 g = spmv_grid(L, kc);
+  dim3 b(SBX, SBY);
+  ProfScope ps(PROF_SPMV, (24.0 + 8.0 * nv) * L * L * L, st);
+  switch (nv) {
+#define CASE(N) \
+  case N: k_spmv<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    default:
+      throw Error(AJ_ERR_ARG, "spmv_dots: nv out of range");
+  }
+  AJ_LAUNCHED();
+}
+
+}  // namespace aj

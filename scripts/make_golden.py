@@ -31,8 +31,10 @@ def main(which):
             res = np.linalg.norm(A @ X - X * lam, axis=0)
             method = "dense numpy.linalg.eigh"
         else:
-            lam, X, res = eigs.si_lanczos_nearest(A, k + 3, sigma, tol=1e-13)
-            method = "plain shift-and-invert Lanczos, splu inner solve"
+            solve = eigs.iterative_solver(A, sigma, L=L, tol=1e-14)
+            lam, X, res = eigs.si_lanczos_nearest(A, k + 3, sigma, tol=1e-12, solve=solve)
+            method = ("plain shift-and-invert Lanczos (full reorth.), inner solves by oracle SQMR + oracle "
+                      f"multilevel ILDL to 1e-14: {solve.stats}")
         dt = time.time() - t0
         normA = float(abs(A).sum(axis=0).max())
         out = dict(config=c, L=L, W=W, seed=seed, hop=hop, sigma=sigma, k=k,

@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Tolerances (DESIGN.md sect. 5):
+  disorder      bit-exact (integer hash -> exact double arithmetic)
+  spmv          max|y - y_ref| <= 1e-14 * max|y_ref|          (BASELINE north_star)
+  precond       same level structure; ||z - z_ref|| <= 1e-8 ||z_ref||
+  sqmr          converged to tol, true residual <= 10 tol
+  multi_dot     <= 1e-13 relative
+  jd_solve      |lambda - lambda_ref| <= 1e-10 ||A||, ||Ax - lambda x|| <= 1e-8 ||A||,
+                subspace angles <= 1e-7 where Davis-Kahan allows it
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import CONFIGS, rand_vec
+from oracle import anderson as an
+from oracle import eigs, mlildl
+from oracle.sqmr import sqmr as oracle_sqmr
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def T(x):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+def N(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def gpu_eps(b, L, W, seed):
+    import torch
+    e = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    b.anderson_build(e, L, W, seed)
+    return e
+
+
+# ---------------------------------------------------------------- disorder
+@pytest.mark.parametrize("L,W,seed", [(3, 16.5, 0), (10, 16.5, 0), (17, 12.0, 5), (50, 16.5, 1), (250, 21.0, 6)])
+def test_disorder_bit_exact(gpu_lib, L, W, seed):
+    e = N(gpu_eps(gpu_lib, L, W, seed))
+    ref = an.disorder(L, W, seed)
+    assert np.array_equal(e.view(np.uint64), ref.view(np.uint64))
+
+
+# ---------------------------------------------------------------- spmv
+@pytest.mark.parametrize("L", [3, 4, 10, 17, 33, 50, 64, 250])
+@pytest.mark.parametrize("hop,sigma", [(-1.0, 0.0), (1.0, 0.37)])
+def test_spmv_parity(gpu_lib, L, hop, sigma):
+    import torch
+    eps = gpu_eps(gpu_lib, L, 16.5, 3)
+    x = rand_vec(L ** 3, 11)
+    y = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    gpu_lib.spmv(y, T(x), eps, L, hop, sigma)
+    ref = an.stencil_apply(L, an.disorder(L, 16.5, 3), x, hop=hop, sigma=sigma)
+    err = np.abs(N(y) - ref).max()
+    assert err <= 1e-14 * np.abs(ref).max()
+
+
+def test_spmv_plane_wave_gpu(gpu_lib):
+    # closed form independent of the oracle: plane wave eigenfunction of the clean stencil
+    import torch
+    L = 12
+    eps = torch.zeros(L ** 3, dtype=torch.float64, device="cuda")
+    s = np.arange(L ** 3)
+    i, j, k = s % L, (s // L) % L, s // (L * L)
+    kv = 2 * np.pi * np.array([1, 3, 5]) / L
+    x = np.cos(kv[0] * i + kv[1] * j + kv[2] * k + 0.2)
+    y = torch.empty_like(eps)
+    gpu_lib.spmv(y, T(x), eps, L, -1.0, 0.0)
+    lam = -2 * np.cos(kv).sum()
+    assert np.abs(N(y) - lam * x).max() < 1e-13
+
+
+# ---------------------------------------------------------------- preconditioner
+def _oracle_precond(L, eps, hop, sigma, p):
+    A = an.matrix(L, eps, hop=hop, sigma=sigma)
+    return mlildl.MultilevelILDL(A, lattice_L=L, kappa=p.kappa, tau_drop=p.tau_drop, tau_strong=p.tau_strong,
+                                 n_coarse_max=p.n_coarse_max, max_levels=p.max_levels, stall_frac=p.stall_frac,
+                                 dense_cap=p.dense_cap)
+
+
+@pytest.mark.parametrize("L,W,seed,hop,sigma", [(8, 16.5, 1, -1.0, 0.0), (12, 16.5, 2, -1.0, 0.0),
+                                                (16, 12.0, 3, 1.0, 0.25), (11, 21.0, 4, -1.0, 0.0),
+                                                (20, 16.5, 5, -1.0, 0.0)])
+def test_precond_parity(gpu_lib, L, W, seed, hop, sigma):
+    import torch
+    p = gpu_lib.default_precond_params(n_coarse_max=200)
+    eps_g = gpu_eps(gpu_lib, L, W, seed)
+    K = gpu_lib.Precond(eps_g, L, hop, sigma, p)
+    info = K.info()
+    eps = an.disorder(L, W, seed)
+    M = _oracle_precond(L, eps, hop, sigma, p)
+    # identical multilevel structure (decisions taken on the same fp64 values)
+    assert info["levels"] == len(M.levels)
+    assert info["level_n"] == [lv.n for lv in M.levels]
+    assert info["level_nF"] == [len(lv.F) for lv in M.levels]
+    assert info["level_pairs"] == [lv.npairs for lv in M.levels]
+    assert info["coarse_n"] == M.coarse_n
+    assert info["level_nnzS"] == [lv.S.nnz for lv in M.levels]
+    for s in (21, 22):
+        r = rand_vec(L ** 3, s)
+        z = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+        K.apply(z, T(r))
+        zr = M.apply(r)
+        assert np.linalg.norm(N(z) - zr) <= 1e-8 * np.linalg.norm(zr)
+    K.free()
+
+
+def test_precond_exactness_limit_gpu(gpu_lib):
+    # no dropping, no kappa bound, true independent sets -> K^{-1} = (A - sigma I)^{-1}
+    import torch
+    L = 6
+    p = gpu_lib.default_precond_params(kappa=1e300, tau_drop=0.0, tau_strong=0.0, n_coarse_max=10, stall_frac=0.0)
+    eps = gpu_eps(gpu_lib, L, 16.5, 1)
+    K = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
+    x = T(rand_vec(L ** 3, 3))
+    ax = torch.empty_like(x)
+    gpu_lib.spmv(ax, x, eps, L, -1.0, 0.0)
+    z = torch.empty_like(x)
+    K.apply(z, ax)
+    assert torch.linalg.norm(z - x) <= 1e-10 * torch.linalg.norm(x)
+    K.free()
+
+
+def test_precond_symmetric_gpu(gpu_lib):
+    import torch
+    L = 20
+    eps = gpu_eps(gpu_lib, L, 16.5, 9)
+    K = gpu_lib.Precond(eps, L, -1.0, 0.0)
+    r1, r2 = T(rand_vec(L ** 3, 1)), T(rand_vec(L ** 3, 2))
+    z1, z2 = torch.empty_like(r1), torch.empty_like(r1)
+    K.apply(z1, r1)
+    K.apply(z2, r2)
+    a, b = float(r2 @ z1), float(r1 @ z2)
+    assert abs(a - b) <= 1e-10 * max(abs(a), abs(b))
+    K.free()
+
+
+# ---------------------------------------------------------------- SQMR
+@pytest.mark.parametrize("L,sigma", [(10, 0.0), (14, 0.5)])
+def test_sqmr_parity(gpu_lib, L, sigma):
+    import torch
+    hop = -1.0
+    p = gpu_lib.default_precond_params(n_coarse_max=200)
+    eps_g = gpu_eps(gpu_lib, L, 16.5, 1)
+    K = gpu_lib.Precond(eps_g, L, hop, sigma, p)
+    b = rand_vec(L ** 3, 5)
+    x = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    x, it, rel, brk = gpu_lib.sqmr_solve(K, x, T(b), eps_g, L, hop, sigma, tol=1e-10, maxit=300)
+    assert not brk and rel <= 1e-10
+    eps = an.disorder(L, 16.5, 1)
+    A = an.matrix(L, eps, hop=hop, sigma=sigma)
+    xr = N(x)
+    assert np.linalg.norm(A @ xr - b) <= 1e-9 * np.linalg.norm(b)
+    M = _oracle_precond(L, eps, hop, sigma, p)
+    xo, ito, relo, _ = oracle_sqmr(lambda v: A @ v, M.apply, b, tol=1e-10, maxit=300)
+    assert abs(it - ito) <= 2
+    assert np.linalg.norm(xr - xo) <= 1e-8 * np.linalg.norm(xo)
+    K.free()
+
+
+def test_sqmr_unpreconditioned_gpu(gpu_lib):
+    import torch
+    L, hop, sigma = 6, -1.0, 3.0
+    eps_g = gpu_eps(gpu_lib, L, 2.0, 1)
+    b = rand_vec(L ** 3, 5)
+    x = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    x, it, rel, brk = gpu_lib.sqmr_solve(None, x, T(b), eps_g, L, hop, sigma, tol=1e-12, maxit=500)
+    A = an.matrix(L, an.disorder(L, 2.0, 1), hop=hop, sigma=sigma)
+    ref = np.linalg.solve(A.toarray(), b)
+    assert np.linalg.norm(N(x) - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- tall-skinny
+def test_multi_dot_and_ortho(gpu_lib):
+    import torch
+    n, m = 100_003, 19
+    Vh = np.random.default_rng(1).standard_normal((m, n))
+    xh = rand_vec(n, 2)
+    V = T(Vh)
+    x = T(xh)
+    out = gpu_lib.multi_dot(V, m, x)
+    ref = Vh @ xh
+    assert np.abs(out - ref).max() <= 1e-13 * np.abs(ref).max() * np.sqrt(n)
+    Q, _ = np.linalg.qr(Vh.T)
+    Qg = T(Q.T)
+    x2, nrm = gpu_lib.ortho_cgs2(x.clone(), Qg, m)
+    xr = N(x2)
+    assert np.abs(Q.T @ xr).max() <= 1e-13
+    assert abs(np.linalg.norm(xr) - 1.0) <= 1e-13
+    proj = xh - Q @ (Q.T @ xh)
+    assert abs(nrm - np.linalg.norm(proj)) <= 1e-12 * np.linalg.norm(proj)
+
+
+# ---------------------------------------------------------------- Jacobi-Davidson
+def _check_eigs(L, W, seed, hop, lam, X, res, lam_ref, X_ref, normA, angle_tol=None, gap=None):
+    assert np.all(np.abs(np.sort(lam) - np.sort(lam_ref)) <= 1e-10 * normA), (lam, lam_ref)
+    assert np.all(res <= 1e-8 * normA)
+    # recompute residuals with the oracle stencil
+    eps = an.disorder(L, W, seed)
+    for i in range(len(lam)):
+        r = an.stencil_apply(L, eps, X[:, i], hop=hop) - lam[i] * X[:, i]
+        assert np.linalg.norm(r) <= 1e-8 * normA
+    G = X.T @ X
+    assert np.abs(G - np.eye(len(lam))).max() <= 1e-8
+    if angle_tol is not None:
+        oi = np.argsort(lam)
+        orf = np.argsort(lam_ref)
+        for a, b in zip(oi, orf):
+            c = abs(X[:, a] @ X_ref[:, b])
+            ang = np.arccos(min(1.0, c))
+            assert ang <= angle_tol, ang
+
+
+def test_jd_config0(gpu_lib):
+    cfg = CONFIGS[0]
+    L, W, seed, hop, k = cfg["L"], cfg["W"], cfg["seed"], cfg["hop"], cfg["k"]
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "eigs_config0.json")))
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    # tol 1e-12 so that Davis-Kahan (angle <= ||r|| / gap) certifies 1e-7 angles
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, 1e-12, eps, L, hop)
+    A = an.matrix(L, an.disorder(L, W, seed), hop=hop)
+    lr, Xr = eigs.dense_nearest(A, k, 0.0)
+    assert np.allclose(lr, gold["eigenvalues"], rtol=0, atol=1e-13)
+    normA = 6 + np.abs(an.disorder(L, W, seed)).max()
+    _check_eigs(L, W, seed, hop, lam, N(X), res, lr, Xr, normA, angle_tol=1e-7)
+    assert st["converged"] == k
+
+
+@pytest.mark.parametrize("L,W,seed,hop,sigma,k", [(8, 16.5, 1, 1.0, 0.0, 5), (11, 12.0, 2, -1.0, 0.5, 3),
+                                                  (12, 21.0, 3, -1.0, -1.0, 1), (6, 16.5, 4, -1.0, 0.0, 4)])
+def test_jd_variants(gpu_lib, L, W, seed, hop, sigma, k):
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    lam, X, res, st = gpu_lib.jd_solve(k, sigma, 1e-11, eps, L, hop)
+    A = an.matrix(L, an.disorder(L, W, seed), hop=hop)
+    lr, Xr = eigs.dense_nearest(A, k, sigma)
+    normA = 6 + np.abs(an.disorder(L, W, seed)).max()
+    _check_eigs(L, W, seed, hop, lam, N(X), res, lr, Xr, normA)
+
+
+def test_jd_config1_l50(gpu_lib):
+    path = os.path.join(ROOT, "tests", "golden", "eigs_config1.json")
+    if not os.path.exists(path):
+        pytest.fail("golden file for config 1 missing (scripts/make_golden.py 1)")
+    gold = json.load(open(path))
+    cfg = CONFIGS[1]
+    L, W, seed, hop, k = cfg["L"], cfg["W"], cfg["seed"], cfg["hop"], cfg["k"]
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop)
+    normA = 6 + np.abs(an.disorder(L, W, seed)).max()
+    lr = np.array(gold["eigenvalues"][:k])
+    assert np.all(np.abs(np.sort(lam) - np.sort(lr)) <= 1e-10 * normA), (lam, lr)
+    assert np.all(res <= 1e-8 * normA)
+    Xh = N(X)
+    e = an.disorder(L, W, seed)
+    for i in range(k):
+        r = an.stencil_apply(L, e, Xh[:, i], hop=hop) - lam[i] * Xh[:, i]
+        assert np.linalg.norm(r) <= 1e-8 * normA
+
+
+def test_jd_host_e2e(gpu_lib):
+    L, W, seed, hop = 10, 16.5, 0, -1.0
+    eps = an.disorder(L, W, seed)
+    Xh = np.zeros((5, L ** 3))
+    lam, res, st = gpu_lib.jd_solve_host(5, 0.0, 1e-10, eps, L, hop, X_host=Xh)
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "eigs_config0.json")))
+    normA = 6 + np.abs(eps).max()
+    assert np.all(np.abs(np.sort(lam) - np.sort(gold["eigenvalues"])) <= 1e-10 * normA)
+    for i in range(5):
+        r = an.stencil_apply(L, eps, Xh[i], hop=hop) - lam[i] * Xh[i]
+        assert np.linalg.norm(r) <= 1e-8 * normA

@@ -48,3 +48,15 @@ def test_dense_residuals():
     lam, X = eigs.dense_nearest(A, 5, 0.0)
     assert np.all(np.abs(lam[:-1]) <= np.abs(lam[1:]) + 1e-15)
     assert np.linalg.norm(A @ X - X * lam) < 1e-12
+
+
+def test_si_lanczos_iterative_inner_matches_dense():
+    # the iterative full-accuracy inner solver (reading R14) gives the dense answer
+    L = 10
+    A = an.matrix(L, an.disorder(L, 16.5, 0), hop=-1.0)
+    solve = eigs.iterative_solver(A, 0.0, L=L, tol=1e-14)
+    ll, Xl, res = eigs.si_lanczos_nearest(A, 5, 0.0, tol=1e-12, solve=solve)
+    ld, Xd = eigs.dense_nearest(A, 5, 0.0)
+    normA = abs(A).sum(axis=0).max()
+    assert np.allclose(ll, ld, atol=1e-12 * normA)
+    assert np.all(res <= 1e-12 * normA)

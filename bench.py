@@ -126,22 +126,33 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(cfg, k, seed):
-    """The oracle as it stands (numpy/scipy, 1 thread) on the same workload, once."""
+CPU_SAMPLE_L = 24
+
+
+def log(*a):
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
+def cpu_baseline(cfg, k, seed, Ls=CPU_SAMPLE_L):
+    """The oracle as it stands (numpy/scipy, 1 thread): one full solve (multilevel ILDL
+    setup + JD, same W, seed, sigma, tol, k) on a bounded L_s^3 sample of the workload,
+    scaled linearly in the number of sites to the workload's L^3."""
     from threadpoolctl import threadpool_limits
 
     from oracle import anderson as an
     from oracle import mlildl
     from oracle.jd import jd_nearest
     L, W, hop, sigma, tol = cfg["L"], cfg["W"], cfg["hop"], cfg["sigma"], cfg["tol"]
+    Ls = min(Ls, L)
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
-        e = an.disorder(L, W, seed)
-        A = an.matrix(L, e, hop=hop)
-        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=1024)
+        e = an.disorder(Ls, W, seed)
+        A = an.matrix(Ls, e, hop=hop)
+        M = mlildl.MultilevelILDL(an.matrix(Ls, e, hop=hop, sigma=sigma), lattice_L=Ls, n_coarse_max=1024)
         lam, X, st = jd_nearest(A, M.apply, k, sigma=sigma, tol=tol)
         dt = time.perf_counter() - t0
-    return dt, lam
+    scale = (L ** 3) / (Ls ** 3)
+    return dt * scale, dt, Ls, scale
 
 
 def run_reference(args, cfg, ws, rank):
@@ -150,7 +161,8 @@ def run_reference(args, cfg, ws, rank):
     k = cfg["k"]
     times = []
     for i in range(args.warmup + args.steps):
-        dt, lam = cpu_baseline(cfg, k, cfg["seed"])
+        dt, raw, Ls, scale = cpu_baseline(cfg, k, cfg["seed"])
+        log(f"reference step {i}: sample {raw:.1f}s x {scale:.2f}")
         if i >= args.warmup:
             times.append(dt)
     v = sum(times) / len(times)
@@ -159,7 +171,9 @@ def run_reference(args, cfg, ws, rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
-                             "sample": "full configs workload per step (oracle JD + oracle multilevel ILDL, numpy, 1 thread)"},
+                             "sample": f"per step: one full oracle solve (oracle/jd.py + oracle/mlildl.py, numpy, 1 "
+                                       f"thread) on L={Ls} with the same W/seed/sigma/tol/k, scaled x{scale:.3f} "
+                                       f"(sites ratio) to L={cfg['L']}"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -243,8 +257,10 @@ def run_ours(args, cfg, ws, rank, local):
     def step():
         return binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], want_vectors=True)
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         lam, X, res, stats = step()
+        log(f"warmup {i}: setup {stats['setup_ms']:.1f} ms solve {stats['solve_ms']:.1f} ms outer {stats['outer']} "
+            f"inner {stats['inner_total']} levels {stats['precond']['levels']}")
     peak, peak_src = peaks()
     torch.cuda.synchronize()
     barrier(ws)
@@ -262,6 +278,7 @@ def run_ours(args, cfg, ws, rank, local):
             e1.record(st)
             e1.synchronize()
             per.append(e0.elapsed_time(e1))
+            log(f"step: {per[-1]:.1f} ms")
         torch.cuda.synchronize()
     barrier(ws)
     torch.cuda.synchronize()
@@ -308,20 +325,25 @@ def run_ours(args, cfg, ws, rank, local):
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * k + 16 * k,
                "api": "jd_solve_host (C ABI, pinned host eps in, eigenvalues/residuals/eigenvectors out)"}
 
+    log("e2e done" if e2e else "e2e skipped")
     kr = None
     if rank == 0 and args.big_L and ws == 1:
         try:
+            log(f"kernel roofline pass at L={args.big_L}")
             kr = big_roofline(binding, args.big_L, peak)
         except Exception as ex:
             kr = {"error": str(ex)[:300]}
 
+    log(f"kernel roofline: {kr}")
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        dt, lam_c = cpu_baseline(cfg, k, seed)
+        dt, raw, Ls, scale = cpu_baseline(cfg, k, seed)
         cpu = {"value": dt, "unit": "s", "cores": 1, "kind": "oracle",
-               "sample": f"one full solve of the same workload (L={L}, k={k}) by oracle/jd.py + oracle/mlildl.py "
-                         f"(numpy/scipy, threadpool limited to 1 thread)",
-               "max_abs_eig_diff_vs_gpu": float(np.max(np.abs(np.sort(lam_c) - np.sort(lam))))}
+               "sample": f"one full oracle solve (oracle/jd.py + oracle/mlildl.py, numpy/scipy, 1 thread) on "
+                         f"L={Ls} (same W, seed, sigma, tol, k) took {raw:.2f} s; scaled x{scale:.3f} by the "
+                         f"sites ratio to L={L} (linear extrapolation; the oracle's per-site cost grows with L, "
+                         f"so this understates it)"}
+        log(f"cpu baseline: {raw:.1f} s sample")
 
     clocks = clk.summary()
     if rank == 0:

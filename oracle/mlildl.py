@@ -45,6 +45,24 @@ class Level:
     pass
 
 
+def _unique_inverse(keys):
+    """np.unique(keys, return_inverse=True) by sorting (numpy's hash-based
+    unique is pathologically slow on large int64 keys)."""
+    keys = np.asarray(keys)
+    order = np.argsort(keys, kind="stable")
+    ks = keys[order]
+    first = np.ones(len(ks), bool)
+    first[1:] = ks[1:] != ks[:-1]
+    uniq = ks[first]
+    inv = np.empty(len(keys), dtype=np.int64)
+    inv[order] = np.cumsum(first) - 1
+    return uniq, inv
+
+
+def _unique(keys):
+    return _unique_inverse(keys)[0]
+
+
 def _scaled(A):
     A = sp.csr_matrix(A)
     A.sort_indices()
@@ -95,24 +113,31 @@ def _pair_candidates(Ah, dg, lmax1, d1, p, kappa):
     mutual = has.copy()
     mutual[has] = p[p[has]] == idx[has]
     cand = np.where(mutual & (idx < p) & ~(ok1 & ok1[np.maximum(p, 0)]))[0]
+    ip, ix, dv = Ah.indptr, Ah.indices, Ah.data
     for i in cand:
         j = int(p[i])
-        aii, ajj, aij = dg[i], dg[j], Ah[i, j]
+        ci, vi = ix[ip[i]:ip[i + 1]], dv[ip[i]:ip[i + 1]]
+        cj, vj = ix[ip[j]:ip[j + 1]], dv[ip[j]:ip[j + 1]]
+        aii, ajj = dg[i], dg[j]
+        aij = vi[np.searchsorted(ci, j)]
         det = aii * ajj - aij * aij
         if det == 0.0:
             continue
         B11, B12, B22 = ajj / det, -aij / det, aii / det
-        ri = Ah.getrow(i).tocoo()
-        rj = Ah.getrow(j).tocoo()
-        ai = dict(zip(ri.col.tolist(), ri.data.tolist()))
-        aj = dict(zip(rj.col.tolist(), rj.data.tolist()))
-        nbrs = sorted((set(ai) | set(aj)) - {i, j})
-        lm2, d2 = 0.0, 0.0
-        for cc in nbrs:
-            aci, acj = ai.get(cc, 0.0), aj.get(cc, 0.0)
-            w = abs(aci * B11 + acj * B12) + abs(aci * B12 + acj * B22)
-            lm2 = max(lm2, w)
-            d2 += w
+        # union of the neighbours of i and j except i, j, ascending
+        nbrs = np.union1d(ci, cj)
+        nbrs = nbrs[(nbrs != i) & (nbrs != j)]
+        ai = np.zeros(len(nbrs))
+        aj = np.zeros(len(nbrs))
+        mi = np.isin(nbrs, ci)
+        mj = np.isin(nbrs, cj)
+        ai[mi] = vi[np.searchsorted(ci, nbrs[mi])]
+        aj[mj] = vj[np.searchsorted(cj, nbrs[mj])]
+        w = np.abs(ai * B11 + aj * B12) + np.abs(ai * B12 + aj * B22)
+        lm2 = float(w.max()) if len(w) else 0.0
+        d2 = 0.0
+        for x in w:                      # sequential sum in ascending column order
+            d2 += x
         lead = i if not ok1[i] else j
         if d2 < d1[lead] and lm2 <= kappa - 1:
             pairs.append((i, j, B11, B12, B22, lm2))
@@ -198,12 +223,12 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
     while True:
         Lfull = _lfull(Ah, inF, partner, b11, b12, dg)
         Lc = Lfull.tocoo()
-        rows_c = Lc.row                     # these are level indices of C nodes
+        rows_c = Lc.row.astype(np.int64)    # level indices of C nodes (int64: n^2 keys)
         lead_of = np.where(partner[Lc.col] >= 0, np.minimum(Lc.col, partner[Lc.col]), Lc.col)
         w = np.abs(Lc.data)
         # aggregate per (c, block)
         key = rows_c * n + lead_of
-        uk, inv = np.unique(key, return_inverse=True)
+        uk, inv = _unique_inverse(key)
         wb = np.zeros(len(uk))
         np.add.at(wb, inv, w)
         bc, bl = uk // n, uk % n
@@ -267,10 +292,10 @@ def _schur(Ah, inF, partner, b11, b12, C, cmap, tau_drop):
     r, c, v = coo.row, coo.col, coo.data
     # entries (c in C, u in F): block leader f = min(u, partner), value to f / to g
     m = (~inF[r]) & inF[c]
-    rc, uc, av = r[m], c[m], v[m]
+    rc, uc, av = r[m].astype(np.int64), c[m].astype(np.int64), v[m]
     lead = np.where(partner[uc] >= 0, np.minimum(uc, partner[uc]), uc)
     key = rc * n + lead
-    uk, inv = np.unique(key, return_inverse=True)
+    uk, inv = _unique_inverse(key)
     acf = np.zeros(len(uk))
     acg = np.zeros(len(uk))
     isf = uc == lead
@@ -301,7 +326,7 @@ def _schur(Ah, inF, partner, b11, b12, C, cmap, tau_drop):
     # starting values a^_cc' on C x C (diagonal always present)
     mc = (~inF[r]) & (~inF[c])
     k0 = cmap[r[mc]] * nC + cmap[c[mc]]
-    keys = np.unique(np.concatenate([k0, tk, np.arange(nC) * (nC + 1)]))
+    keys = _unique(np.concatenate([k0, tk, np.arange(nC) * (nC + 1)]))
     sval = np.zeros(len(keys))
     sval[np.searchsorted(keys, k0)] = v[mc]
     ot = np.lexsort((f, tk))                         # per entry: ascending leader

@@ -37,7 +37,24 @@ def parse():
     ap.add_argument("--big-L", type=int, default=250, help="lattice for the SpMV/precond HBM roofline pass (0=off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # tuning knobs (defaults = library defaults, aj_*_default_params)
+    for k in ["kappa", "tau_drop", "tau_strong", "inner_tol", "switch_tol"]:
+        ap.add_argument("--" + k.replace("_", "-"), type=float, default=None)
+    for k in ["n_coarse_max", "max_levels", "inner_max", "jmin", "jmax"]:
+        ap.add_argument("--" + k.replace("_", "-"), type=int, default=None)
     return ap.parse_args()
+
+
+def params_from_args(binding, args):
+    pp = binding.default_precond_params()
+    jp = binding.default_jd_params()
+    for k in ["kappa", "tau_drop", "tau_strong", "n_coarse_max", "max_levels"]:
+        if getattr(args, k) is not None:
+            setattr(pp, k, getattr(args, k))
+    for k in ["inner_tol", "switch_tol", "inner_max", "jmin", "jmax"]:
+        if getattr(args, k) is not None:
+            setattr(jp, k, getattr(args, k))
+    return pp, jp
 
 
 def dist_setup(args):
@@ -254,8 +271,11 @@ def run_ours(args, cfg, ws, rank, local):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream()
 
+    pp, jp = params_from_args(binding, args)
+
     def step():
-        return binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], want_vectors=True)
+        return binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp,
+                                want_vectors=True)
 
     for i in range(args.warmup):
         lam, X, res, stats = step()
@@ -311,13 +331,14 @@ def run_ours(args, cfg, ws, rank, local):
         eps_h.copy_(eps.cpu())
         X_h = torch.empty((k, n), dtype=torch.float64, pin_memory=True)
         eh, Xh = eps_h.numpy(), X_h.numpy()
-        binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], X_host=Xh)  # warm
+        binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], pparams=pp, jparams=jp, X_host=Xh)
         tt = []
         for _ in range(args.steps):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            lam_h, res_h, _ = binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], X_host=Xh)
+            lam_h, res_h, _ = binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], pparams=pp,
+                                                    jparams=jp, X_host=Xh)
             e1.record(st)
             e1.synchronize()
             tt.append(e0.elapsed_time(e1))
@@ -357,7 +378,8 @@ def run_ours(args, cfg, ws, rank, local):
                        "setup_ms": stats["setup_ms"], "solve_ms": stats["solve_ms"],
                        "max_resid_rel": float(np.max(res)) / (6 * abs(cfg["hop"]) + float(eps.abs().max())),
                        "eigenvalues": [float(v) for v in lam]},
-                "step_ms": per}
+                "step_ms": per,
+                "params": {f: getattr(pp, f) for f, _ in pp._fields_} | {f: getattr(jp, f) for f, _ in jp._fields_}}
         print(json.dumps(line), flush=True)
 
 

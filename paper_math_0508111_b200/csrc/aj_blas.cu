@@ -81,6 +81,14 @@ int num_sms() {
     int dev = 0;
     AJ_CUDA(cudaGetDevice(&dev));
     AJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // keep freed stream-ordered allocations mapped: the factorisation allocates and
+    // frees GBs per level, and the default threshold (0) would unmap them at every
+    // synchronisation and remap them at the next cudaMallocAsync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
   }
   return sms;
 }

@@ -207,7 +207,7 @@ void aj_jd_default_params(aj_jd_params* p) {
   p->jmax = 25;
   p->max_outer = 2000;
   p->inner_max = 60;
-  p->inner_tol = 0.1;
+  p->inner_tol = 3e-3;
   p->switch_tol = 1e-3;
   p->seed = 7;
   p->verbose = 0;

@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -392,12 +394,13 @@ __global__ void k_cflags(int n, const int8_t* __restrict__ inF, int32_t* __restr
   for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) flag[i] = inF[i] ? 0 : 1;
 }
 __global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __restrict__ scan,
-                       int32_t* __restrict__ cmap, int32_t* __restrict__ cidx,
+                       int32_t* __restrict__ cmap, int32_t* __restrict__ cidx, int32_t* __restrict__ fidx,
                        int32_t* __restrict__ partner_out, const int32_t* __restrict__ partner,
                        double* __restrict__ b11, double* __restrict__ b12) {
   for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
     if (inF[i]) {
       cmap[i] = -1;
+      fidx[i - scan[i]] = i;  // scan counts the C nodes before i
       partner_out[i] = partner[i];
     } else {
       cmap[i] = scan[i];
@@ -441,72 +444,79 @@ __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t
   }
 }
 
-// L^T rows (F node u): entries (cmap[c], l_cu) over C nodes c adjacent to u or its partner
+// L^T rows (F index f' -> node u = fidx[f']): entries (cmap[c], l_cu) over C nodes c
+// adjacent to u or its partner
 template <bool FILL>
-__global__ void k_LT_rows(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                          const double* __restrict__ ah, const int8_t* __restrict__ inF,
-                          const int32_t* __restrict__ partner, const double* __restrict__ b11,
-                          const double* __restrict__ b12, const int32_t* __restrict__ cmap, double tau,
-                          int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ LTcol,
-                          double* __restrict__ LTval) {
-  for (int u = blockIdx.x * TB + threadIdx.x; u < n; u += gridDim.x * TB) {
-    int64_t w = FILL ? cnt_or_ptr[u] : 0;
-    if (inF[u]) {
-      const int32_t p = partner[u];
-      if (p < 0) {
-        for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
-          const int32_t c = col[e];
-          if (c == u || inF[c]) continue;
-          const double l = __dmul_rn(ah[e], b11[u]);
-          if (fabs(l) >= tau) {
-            if (FILL) {
-              LTcol[w] = cmap[c];
-              LTval[w] = l;
-            }
-            ++w;
+__global__ void k_LT_rows(int nF, const int32_t* __restrict__ fidx, const int64_t* __restrict__ ptr,
+                          const int32_t* __restrict__ col, const double* __restrict__ ah,
+                          const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
+                          const double* __restrict__ b11, const double* __restrict__ b12,
+                          const int32_t* __restrict__ cmap, double tau, int64_t* __restrict__ cnt_or_ptr,
+                          int32_t* __restrict__ LTcol, double* __restrict__ LTval) {
+  for (int fp = blockIdx.x * TB + threadIdx.x; fp < nF; fp += gridDim.x * TB) {
+    const int u = fidx[fp];
+    int64_t w = FILL ? cnt_or_ptr[fp] : 0;
+    const int32_t p = partner[u];
+    if (p < 0) {
+      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+        const int32_t c = col[e];
+        if (c == u || inF[c]) continue;
+        const double l = __dmul_rn(ah[e], b11[u]);
+        if (fabs(l) >= tau) {
+          if (FILL) {
+            LTcol[w] = cmap[c];
+            LTval[w] = l;
           }
+          ++w;
         }
-      } else {
-        const int32_t f = min(u, p), g = max(u, p);
-        int64_t ef = ptr[f], eg = ptr[g];
-        const int64_t ef1 = ptr[f + 1], eg1 = ptr[g + 1];
-        while (ef < ef1 || eg < eg1) {
-          const int32_t cf = (ef < ef1) ? col[ef] : INT32_MAX;
-          const int32_t cg = (eg < eg1) ? col[eg] : INT32_MAX;
-          const int32_t c = min(cf, cg);
-          double a_cf = 0.0, a_cg = 0.0;
-          if (cf == c) a_cf = ah[ef++];
-          if (cg == c) a_cg = ah[eg++];
-          if (c == f || c == g || inF[c]) continue;
-          const double l = (u == f) ? lval_pair(a_cf, a_cg, b11[f], b12[g])
-                                    : lval_pair(a_cf, a_cg, b12[f], b11[g]);
-          if (fabs(l) >= tau) {
-            if (FILL) {
-              LTcol[w] = cmap[c];
-              LTval[w] = l;
-            }
-            ++w;
+      }
+    } else {
+      const int32_t f = min(u, p), g = max(u, p);
+      int64_t ef = ptr[f], eg = ptr[g];
+      const int64_t ef1 = ptr[f + 1], eg1 = ptr[g + 1];
+      while (ef < ef1 || eg < eg1) {
+        const int32_t cf = (ef < ef1) ? col[ef] : INT32_MAX;
+        const int32_t cg = (eg < eg1) ? col[eg] : INT32_MAX;
+        const int32_t c = min(cf, cg);
+        double a_cf = 0.0, a_cg = 0.0;
+        if (cf == c) a_cf = ah[ef++];
+        if (cg == c) a_cg = ah[eg++];
+        if (c == f || c == g || inF[c]) continue;
+        const double l = (u == f) ? lval_pair(a_cf, a_cg, b11[f], b12[g]) : lval_pair(a_cf, a_cg, b12[f], b11[g]);
+        if (fabs(l) >= tau) {
+          if (FILL) {
+            LTcol[w] = cmap[c];
+            LTval[w] = l;
           }
+          ++w;
         }
       }
     }
-    if (!FILL) cnt_or_ptr[u] = w;
+    if (!FILL) cnt_or_ptr[fp] = w;
   }
 }
 
 // ----------------------------------------------------------------------------
 // Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, symmetric by construction,
 // off-diagonals with |s| < tau dropped.  One warp per coarse row.
-constexpr int SW = 4;           // warps per CTA
-constexpr int BMAX = 96;        // F blocks adjacent to one row
-constexpr int HT = 4096;        // per-warp hash set of candidate columns (power of 2)
+constexpr int SW = 4;            // warps per CTA
+constexpr int BMAX = 96;         // F blocks adjacent to one row (shared-memory variant)
+constexpr int HT = 2048;         // per-warp hash table, shared-memory variant (power of 2)
+constexpr int HTG = 32768;       // per-warp hash table, global-memory fallback variant
+constexpr int BMAXG = 2048;      // block list of the fallback variant
 struct BlkEnt {
   int32_t f, g, lead;
   double acf, acg, Bff, Bgg, Bfg;
 };
-constexpr size_t kSchurSmem = (size_t)SW * (HT * sizeof(int32_t) + BMAX * sizeof(BlkEnt));
+constexpr size_t kSchurSmem = (size_t)SW * (HT * sizeof(int32_t) + HT * sizeof(double) + BMAX * sizeof(BlkEnt));
+// global scratch per warp: list/keys (T int32) + values (T doubles) [+ table for the fallback]
+template <int T, bool GLOBAL>
+constexpr size_t schur_scratch_words() {
+  return GLOBAL ? (size_t)T * (1 + 2 + 1 + 2) + (size_t)BMAXG * (sizeof(BlkEnt) / 4) : (size_t)T * 3;
+}
 
-__device__ __forceinline__ void warp_bitonic_sort(int32_t* a, int P) {
+// bitonic sort of (key, value) pairs by key, one warp
+__device__ __forceinline__ void warp_bitonic_sort_kv(int32_t* a, double* v, int P) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -518,6 +528,9 @@ __device__ __forceinline__ void warp_bitonic_sort(int32_t* a, int P) {
           if ((x > y) == up) {
             a[t] = y;
             a[ixj] = x;
+            const double tv = v[t];
+            v[t] = v[ixj];
+            v[ixj] = tv;
           }
         }
       }
@@ -526,53 +539,90 @@ __device__ __forceinline__ void warp_bitonic_sort(int32_t* a, int P) {
   }
 }
 
-// insert key into the warp's open-addressing set; counts new keys in *cnt
-__device__ __forceinline__ void hset_insert(int32_t* tab, int32_t key, int* cnt) {
-  uint32_t h = ((uint32_t)key * 2654435761u) & (HT - 1);
-  for (int probe = 0; probe < HT; ++probe) {
+// find-or-insert `key` into a warp's table of size T (power of 2); returns the
+// slot or -1 when full.  New keys get value 0 and their slot appended to `list`.
+template <int T>
+__device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int* cnt, int32_t* list) {
+  constexpr int BITS = (T == 2048) ? 11 : 15;
+  static_assert(T == 2048 || T == 32768, "table size");
+  uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
+  for (int probe = 0; probe < T; ++probe) {
     const int32_t prev = atomicCAS(&tab[h], -1, key);
     if (prev == -1) {
-      atomicAdd(cnt, 1);
-      return;
+      val[h] = 0.0;
+      const int pos = atomicAdd(cnt, 1);
+      if (pos < T) list[pos] = (int32_t)h;
+      return (int)h;
     }
-    if (prev == key) return;
-    h = (h + 1) & (HT - 1);
+    if (prev == key) return (int)h;
+    h = (h + 1) & (T - 1);
   }
+  return -1;
 }
 
-// Schur complement S = A^_CC - A^_CF B^{-1} A^_FC (reading R10: ascending-leader
-// accumulation of the symmetric block terms, bitwise symmetric), off-diagonals
-// with |s| < tau dropped.  One warp per coarse row.
-template <bool FILL>
+// Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, scatter form (reading R10):
+// s_cc' starts at a^_cc', then the F blocks adjacent to c are applied one after
+// the other in ascending leader order; block b walks the rows of its members and
+// subtracts T_b(c, c') from the slot of every coarse neighbour c' (each c' once
+// per block, so lanes never share a slot inside a block).  The per-entry order
+// is ascending leader -- the oracle's order, bitwise symmetric in (c, c').
+// Off-diagonals |s| < tau are dropped.  One warp per coarse row.
+// GLOBAL = false: tables in shared memory (T = 2048); rows that do not fit are
+// flagged in row_ovf and queued in ovf_list.  GLOBAL = true: the fallback over
+// ovf_list with T = 32768 tables in global memory.
+template <bool FILL, bool GLOBAL>
 __global__ void __launch_bounds__(SW * 32)
-    k_schur(int nC, const int32_t* __restrict__ cidx, const int32_t* __restrict__ cmap,
-            const int64_t* __restrict__ ptr, const int32_t* __restrict__ col, const double* __restrict__ ah,
-            const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
+    k_schur(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
+            const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+            const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
             const double* __restrict__ b11, const double* __restrict__ b12, double tau,
             int32_t* __restrict__ scratch_all, int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ Scol,
-            double* __restrict__ Sval, int* __restrict__ overflow) {
+            double* __restrict__ Sval, int8_t* __restrict__ row_ovf, int32_t* __restrict__ ovf_list,
+            int* __restrict__ ovf_count, int* __restrict__ error) {
+  constexpr int T = GLOBAL ? HTG : HT;
+  constexpr int BM = GLOBAL ? BMAXG : BMAX;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int scount[SW], sbcount[SW], sccount[SW];
+  __shared__ int scount[SW], sbcount[SW];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (size_t)wid * HT;
-  BlkEnt* blk = reinterpret_cast<BlkEnt*>(smem_raw + (size_t)SW * HT * sizeof(int32_t)) + (size_t)wid * BMAX;
-  int32_t* scratch = scratch_all + (size_t)(blockIdx.x * SW + wid) * HT;
-  for (int cp = blockIdx.x * SW + wid; cp < nC; cp += gridDim.x * SW) {
+  int32_t* wscr = scratch_all + (size_t)(blockIdx.x * SW + wid) * schur_scratch_words<T, GLOBAL>();
+  int32_t* list = wscr;                                         // T int32
+  double* kvals = reinterpret_cast<double*>(wscr + T);          // T doubles
+  double* vals;
+  int32_t* tab;
+  BlkEnt* blk;
+  if constexpr (GLOBAL) {
+    tab = wscr + 3 * T;                                         // T int32
+    vals = reinterpret_cast<double*>(wscr + 4 * T);             // T doubles
+    blk = reinterpret_cast<BlkEnt*>(wscr + 6 * T);
+  } else {
+    vals = reinterpret_cast<double*>(smem_raw) + (size_t)wid * T;
+    tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)SW * T * sizeof(double)) + (size_t)wid * T;
+    blk = reinterpret_cast<BlkEnt*>(smem_raw + (size_t)SW * T * (sizeof(double) + sizeof(int32_t))) +
+          (size_t)wid * BM;
+  }
+  for (int t = lane; t < T; t += 32) tab[t] = -1;  // reset incrementally after each row
+  __syncwarp();
+  for (int ri = blockIdx.x * SW + wid; ri < nrows; ri += gridDim.x * SW) {
+    const int cp = rowlist ? rowlist[ri] : ri;
+    if (!GLOBAL && FILL && row_ovf[cp]) continue;  // done by the fallback
     const int c = cidx[cp];
     const int64_t lo = ptr[c], hi = ptr[c + 1];
     __syncwarp();
-    for (int t = lane; t < HT; t += 32) tab[t] = -1;
     if (lane == 0) {
       scount[wid] = 0;
       sbcount[wid] = 0;
-      sccount[wid] = 0;
     }
     __syncwarp();
-    // phase 1: own coarse neighbours + F blocks of row c
+    bool full = false;
+    // (1) s_cc' = a^_cc' for the coarse neighbours of c; collect the F blocks of row c
     for (int64_t e = lo + lane; e < hi; e += 32) {
       const int32_t u = col[e];
       if (!inF[u]) {
-        hset_insert(tab, cmap[u], &scount[wid]);
+        const int sl = hslot<T>(tab, vals, cmap[u], &scount[wid], list);
+        if (sl < 0)
+          full = true;
+        else
+          vals[sl] = ah[e];
       } else {
         const int32_t p = partner[u];
         bool take = true;
@@ -584,7 +634,7 @@ __global__ void __launch_bounds__(SW * 32)
         }
         if (take) {
           const int bpos = atomicAdd(&sbcount[wid], 1);
-          if (bpos < BMAX) {
+          if (bpos < BM) {
             BlkEnt bb;
             if (p < 0) {
               bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
@@ -602,14 +652,10 @@ __global__ void __launch_bounds__(SW * 32)
     }
     __syncwarp();
     const int nb = sbcount[wid];
-    if (nb > BMAX) {
-      if (lane == 0) atomicExch(overflow, 1);
-      continue;
-    }
-    if (lane == 0) {  // blocks in ascending leader order (insertion sort, nb small)
-      for (int a = 1; a < nb; ++a) {
-        BlkEnt v = blk[a];
-        int q = a - 1;
+    if (lane == 0 && nb <= BM) {  // blocks in ascending leader order (insertion sort)
+      for (int a2 = 1; a2 < nb; ++a2) {
+        BlkEnt v = blk[a2];
+        int q = a2 - 1;
         while (q >= 0 && blk[q].lead > v.lead) {
           blk[q + 1] = blk[q];
           --q;
@@ -618,37 +664,85 @@ __global__ void __launch_bounds__(SW * 32)
       }
     }
     __syncwarp();
-    // phase 2: coarse neighbours of every block member
-    for (int bi = 0; bi < nb; ++bi) {
-      for (int mm = 0; mm < 2; ++mm) {
-        const int32_t u = (mm == 0) ? blk[bi].f : blk[bi].g;
-        if (u < 0) continue;
-        for (int64_t e = ptr[u] + lane; e < ptr[u + 1]; e += 32) {
-          const int32_t v = col[e];
-          if (!inF[v]) hset_insert(tab, cmap[v], &scount[wid]);
+    // (2) subtract the block terms, block after block
+    if (nb <= BM) {
+      for (int bi = 0; bi < nb && !__any_sync(0xffffffffu, full); ++bi) {
+        const BlkEnt B = blk[bi];
+        if (B.g < 0) {
+          for (int64_t e = ptr[B.f] + lane; e < ptr[B.f + 1]; e += 32) {
+            const int32_t v = col[e];
+            if (inF[v]) continue;
+            const int sl = hslot<T>(tab, vals, cmap[v], &scount[wid], list);
+            if (sl < 0) {
+              full = true;
+              continue;
+            }
+            vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
+          }
+        } else {
+          // rows f and g: entries of f (with a_{c'g} looked up in g), then entries only in g
+          const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
+          for (int pass = 0; pass < 2; ++pass) {
+            const int64_t s0 = pass ? g0 : f0, s1 = pass ? g1 : f1;
+            for (int64_t e = s0 + lane; e < s1; e += 32) {
+              const int32_t v = col[e];
+              if (inF[v]) continue;
+              double a2f, a2g;
+              if (pass == 0) {
+                a2f = ah[e];
+                const int64_t eg = lookup_idx(col, g0, g1, v);
+                a2g = (eg >= 0) ? ah[eg] : 0.0;
+              } else {
+                if (lookup_idx(col, f0, f1, v) >= 0) continue;  // handled in pass 0
+                a2f = 0.0;
+                a2g = ah[e];
+              }
+              const int sl = hslot<T>(tab, vals, cmap[v], &scount[wid], list);
+              if (sl < 0) {
+                full = true;
+                continue;
+              }
+              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
+                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
+              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
+              vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
+            }
+          }
         }
+        __syncwarp();
       }
-      if (scount[wid] > (HT * 3) / 4) break;
+    }
+    const int nc = min(scount[wid], T);
+    const bool bad = (nb > BM) || __any_sync(0xffffffffu, full) || scount[wid] > (T * 3) / 4;
+    // (3) collect (key, value) through the slot list and reset those slots
+    int32_t* keys = list;
+    for (int t = lane; t < nc; t += 32) {
+      const int32_t sl = list[t];
+      const int32_t kk = tab[sl];
+      kvals[t] = vals[sl];
+      tab[sl] = -1;
+      keys[t] = kk;
     }
     __syncwarp();
-    const int nc = scount[wid];
-    if (nc > (HT * 3) / 4) {
-      if (lane == 0) atomicExch(overflow, 2);
+    if (bad) {
+      if (GLOBAL) {
+        if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
+      } else if (!FILL && lane == 0) {
+        row_ovf[cp] = 1;
+        ovf_list[atomicAdd(ovf_count, 1)] = cp;
+        cnt_or_ptr[cp] = 0;
+      }
       continue;
     }
-    // compact the set into scratch, then back into smem and sort
-    for (int t = lane; t < HT; t += 32) {
-      const int32_t kk = tab[t];
-      if (kk >= 0) scratch[atomicAdd(&sccount[wid], 1)] = kk;
-    }
-    __syncwarp();
     int P = 1;
     while (P < nc) P <<= 1;
-    for (int t = lane; t < P; t += 32) tab[t] = (t < nc) ? scratch[t] : INT32_MAX;
+    for (int t = lane; t < P; t += 32) {  // sort in the (now empty) table storage
+      tab[t] = (t < nc) ? keys[t] : INT32_MAX;
+      vals[t] = (t < nc) ? kvals[t] : 0.0;
+    }
     __syncwarp();
-    warp_bitonic_sort(tab, P);
-    // phase 3: values of the unique columns, ascending, chunks of 32
-    int64_t wbase = FILL ? cnt_or_ptr[cp] : 0;
+    warp_bitonic_sort_kv(tab, vals, P);
+    const int64_t wbase = FILL ? cnt_or_ptr[cp] : 0;
     int kept = 0;
     for (int t0 = 0; t0 < nc; t0 += 32) {
       const int t = t0 + lane;
@@ -657,24 +751,7 @@ __global__ void __launch_bounds__(SW * 32)
       double sv = 0.0;
       if (t < nc) {
         c2p = tab[t];
-        const int32_t c2 = cidx[c2p];
-        sv = lookup(col, ah, lo, hi, c2);
-        const int64_t lo2 = ptr[c2], hi2 = ptr[c2 + 1];
-        for (int bi = 0; bi < nb; ++bi) {
-          const BlkEnt& B = blk[bi];
-          const double a2f = lookup(col, ah, lo2, hi2, B.f);
-          if (B.g < 0) {
-            if (a2f != 0.0) sv = __dsub_rn(sv, __dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)));
-          } else {
-            const double a2g = lookup(col, ah, lo2, hi2, B.g);
-            if (a2f != 0.0 || a2g != 0.0) {
-              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
-                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
-              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
-              sv = __dsub_rn(sv, __dadd_rn(t1, t2));
-            }
-          }
-        }
+        sv = vals[t];
         keep = (c2p == cp) || (fabs(sv) >= tau);
       }
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -686,6 +763,9 @@ __global__ void __launch_bounds__(SW * 32)
       kept += __popc(bal);
     }
     if (!FILL && lane == 0) cnt_or_ptr[cp] = kept;
+    __syncwarp();
+    for (int t = lane; t < P; t += 32) tab[t] = -1;  // the table is empty again
+    __syncwarp();
   }
 }
 
@@ -767,37 +847,96 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 }
 
 // ----------------------------------------------------------------------------
-// application kernels
-__global__ void k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
-                            const double* __restrict__ r, const int64_t* __restrict__ Lptr,
-                            const int32_t* __restrict__ Lcol, const double* __restrict__ Lval,
-                            double* __restrict__ rn) {
-  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
+// application kernels: G threads per row (G | 32), coalesced row segments,
+// shuffle reduction inside the group.  One row per group, no grid-stride
+// loop so every lane of a warp reaches the shuffles.
+template <int G>
+__global__ void __launch_bounds__(TB)
+    k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
+                const double* __restrict__ r, const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol,
+                const double* __restrict__ Lval, double* __restrict__ rn) {
+  const int gid = blockIdx.x * TB + threadIdx.x;
+  const int cp = gid / G, lane = gid % G;
+  const bool act = cp < nC;
+  double acc = 0.0;
+  if (act) {
+    const int64_t e1 = Lptr[cp + 1];
+    for (int64_t e = Lptr[cp] + lane; e < e1; e += G) acc += Lval[e] * __ldg(&r[Lcol[e]]);
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (act && lane == 0) {
     const int c = cidx[cp];
-    double acc = D[c] * r[c];
-    for (int64_t e = Lptr[cp]; e < Lptr[cp + 1]; ++e) acc -= Lval[e] * r[Lcol[e]];
-    rn[cp] = acc;
+    rn[cp] = D[c] * r[c] - acc;
   }
 }
-__global__ void k_apply_bwd(int n, const int32_t* __restrict__ cmap, const double* __restrict__ D,
-                            const double* __restrict__ r, const int32_t* __restrict__ partner,
-                            const double* __restrict__ b11, const double* __restrict__ b12,
-                            const int64_t* __restrict__ LTptr, const int32_t* __restrict__ LTcol,
-                            const double* __restrict__ LTval, const double* __restrict__ zn,
-                            double* __restrict__ z) {
-  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
-    const int32_t cm = cmap[i];
-    if (cm >= 0) {
-      z[i] = D[i] * zn[cm];
-    } else {
-      double acc = b11[i] * (D[i] * r[i]);
-      const int32_t p = partner[i];
-      if (p >= 0) acc += b12[i] * (D[p] * r[p]);
-      for (int64_t e = LTptr[i]; e < LTptr[i + 1]; ++e) acc -= LTval[e] * zn[LTcol[e]];
-      z[i] = D[i] * acc;
+
+// backward substitution: blocks [0, bF) take the pivot (F) rows with G lanes
+// each, blocks [bF, ...) copy the coarse solution back (z_c = D_c zn_c').
+template <int G>
+__global__ void __launch_bounds__(TB)
+    k_apply_bwd(int nF, int nC, int bF, const int32_t* __restrict__ fidx, const int32_t* __restrict__ cidx,
+                const double* __restrict__ D, const double* __restrict__ r, const int32_t* __restrict__ partner,
+                const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ LTptr,
+                const int32_t* __restrict__ LTcol, const double* __restrict__ LTval, const double* __restrict__ zn,
+                double* __restrict__ z) {
+  if ((int)blockIdx.x >= bF) {
+    const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
+    if (cp < nC) {
+      const int i = cidx[cp];
+      z[i] = D[i] * zn[cp];
     }
+    return;
+  }
+  const int gid = blockIdx.x * TB + threadIdx.x;
+  const int fp = gid / G, lane = gid % G;
+  const bool act = fp < nF;
+  double acc = 0.0;
+  if (act) {
+    const int64_t e1 = LTptr[fp + 1];
+    for (int64_t e = LTptr[fp] + lane; e < e1; e += G) acc += LTval[e] * __ldg(&zn[LTcol[e]]);
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (act && lane == 0) {
+    const int i = fidx[fp];
+    double y = b11[i] * (D[i] * r[i]);
+    const int32_t p = partner[i];
+    if (p >= 0) y += b12[i] * (D[p] * r[p]);
+    z[i] = D[i] * (y - acc);
   }
 }
+
+static int pick_group(double avg_len) {
+  int g = 1;
+  while (g < 32 && g * 2 <= avg_len) g <<= 1;  // ~2 entries per lane
+  return g;
+}
+
+static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t st) {
+  if (v.nC == 0) return;
+  const int G = v.gf;
+  const int grid = std::max(1, ceil_div((int64_t)v.nC * G, TB));
+  switch (G) {
+#define F(GG) case GG: k_apply_fwd<GG><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, v.Lval, rn); break;
+    F(1) F(2) F(4) F(8) F(16) F(32)
+#undef F
+  }
+  AJ_LAUNCHED();
+}
+static void launch_bwd(const Level& v, const double* r, const double* zn, double* z, cudaStream_t st) {
+  const int G = v.gb;
+  const int bF = ceil_div((int64_t)v.nF * G, TB);
+  const int grid = std::max(1, bF + ceil_div(v.nC, TB));
+  switch (G) {
+#define B(GG) case GG: k_apply_bwd<GG><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11, \
+                                                         v.b12, v.LTptr, v.LTcol, v.LTval, zn, z); break;
+    B(1) B(2) B(4) B(8) B(16) B(32)
+#undef B
+  }
+  AJ_LAUNCHED();
+}
+
 // z = G r (dense, warp per row)
 __global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __restrict__ r,
                            double* __restrict__ z) {
@@ -812,13 +951,6 @@ __global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __
 
 // ============================================================================
 // host side
-static void exclusive_scan_i64(const int64_t* in, int64_t* out, int n, cudaStream_t st) {
-  size_t tmp = 0;
-  AJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
-  void* t = dalloc<char>(tmp, st);
-  AJ_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, st));
-  dfree(t, st);
-}
 static void exclusive_scan_i32(const int32_t* in, int32_t* out, int n, cudaStream_t st) {
   size_t tmp = 0;
   AJ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
@@ -833,22 +965,17 @@ static T read_scalar(const T* d, cudaStream_t st) {
   AJ_CUDA(cudaStreamSynchronize(st));
   return h;
 }
-// counts (n) -> ptr (n+1) with total; returns total
+// counts (n) -> ptr (n+1) with total (one device->host read); returns total
 static int64_t counts_to_ptr(int64_t* cnt, int64_t*& ptr, int n, cudaStream_t st) {
   ptr = dalloc<int64_t>((size_t)n + 1, st);
-  if (n == 0) {
-    AJ_CUDA(cudaMemsetAsync(ptr, 0, sizeof(int64_t), st));
-    return 0;
-  }
-  exclusive_scan_i64(cnt, ptr, n, st);
-  int64_t last_c, last_p;
-  AJ_CUDA(cudaMemcpyAsync(&last_c, cnt + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  AJ_CUDA(cudaMemcpyAsync(&last_p, ptr + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  AJ_CUDA(cudaStreamSynchronize(st));
-  const int64_t tot = last_c + last_p;
-  AJ_CUDA(cudaMemcpyAsync(ptr + n, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  AJ_CUDA(cudaStreamSynchronize(st));
-  return tot;
+  AJ_CUDA(cudaMemsetAsync(ptr, 0, sizeof(int64_t), st));
+  if (n == 0) return 0;
+  size_t tmp = 0;
+  AJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt, ptr + 1, n, st));
+  void* t = dalloc<char>(tmp, st);
+  AJ_CUDA(cub::DeviceScan::InclusiveSum(t, tmp, cnt, ptr + 1, n, st));
+  dfree(t, st);
+  return read_scalar(ptr + n, st);
 }
 
 void Csr::release(cudaStream_t st) {
@@ -861,7 +988,7 @@ void Csr::release(cudaStream_t st) {
 }
 
 void Level::release(cudaStream_t st) {
-  for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)partner, (void*)b11, (void*)b12, (void*)Lptr,
+  for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)fidx, (void*)partner, (void*)b11, (void*)b12, (void*)Lptr,
                   (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)r, (void*)z})
     dfree(p, st);
 }
@@ -988,6 +1115,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   lv.cmap = dalloc<int32_t>(n, st);
   lv.cidx = dalloc<int32_t>(std::max(nC, 1), st);
   lv.partner = dalloc<int32_t>(n, st);
+  lv.fidx = dalloc<int32_t>(std::max(nF, 1), st);
   {
     int32_t* flag = dalloc<int32_t>(n, st);
     int32_t* scan = dalloc<int32_t>(n, st);
@@ -995,7 +1123,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     AJ_LAUNCHED();
     exclusive_scan_i32(flag, scan, n, st);
     // b11/b12 of C nodes zeroed inside k_cmap (they were block data of non-F nodes)
-    k_cmap<<<g, TB, 0, st>>>(n, inF, scan, lv.cmap, lv.cidx, lv.partner, partner, b11, b12);
+    k_cmap<<<g, TB, 0, st>>>(n, inF, scan, lv.cmap, lv.cidx, lv.fidx, lv.partner, partner, b11, b12);
     AJ_LAUNCHED();
     dfree(flag, st);
     dfree(scan, st);
@@ -1015,17 +1143,18 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     AJ_LAUNCHED();
     dfree(cnt, st);
   }
-  // L^T (backward) rows over level nodes
+  // L^T (backward) rows over the pivot (F) nodes, in F order
   {
-    int64_t* cnt = dalloc<int64_t>(n, st);
-    k_LT_rows<false><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap, P.tau_drop,
-                                        cnt, nullptr, nullptr);
+    int64_t* cnt = dalloc<int64_t>(nF, st);
+    const int gF = grid_for(nF);
+    k_LT_rows<false><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
+                                         P.tau_drop, cnt, nullptr, nullptr);
     AJ_LAUNCHED();
-    lv.nnzLT = counts_to_ptr(cnt, lv.LTptr, n, st);
+    lv.nnzLT = counts_to_ptr(cnt, lv.LTptr, nF, st);
     lv.LTcol = dalloc<int32_t>(lv.nnzLT, st);
     lv.LTval = dalloc<double>(lv.nnzLT, st);
-    k_LT_rows<true><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap, P.tau_drop,
-                                       lv.LTptr, lv.LTcol, lv.LTval);
+    k_LT_rows<true><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
+                                        P.tau_drop, lv.LTptr, lv.LTcol, lv.LTval);
     AJ_LAUNCHED();
     dfree(cnt, st);
   }
@@ -1033,31 +1162,59 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   {
     S.n = nC;
     int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
-    const int nwarps_total = std::min(ceil_div(std::max(nC, 1), 1), num_sms() * 16 * SW);
+    const int nwarps_total = std::min(std::max(nC, 1), num_sms() * 8 * SW);
     const int gs = std::max(1, ceil_div(nwarps_total, SW));
-    int32_t* cand = dalloc<int32_t>((size_t)gs * SW * HT, st);
+    const int gsg = std::min(gs, num_sms());  // fallback grid (large global tables)
+    int32_t* scr = dalloc<int32_t>((size_t)gs * SW * schur_scratch_words<HT, false>(), st);
+    int8_t* row_ovf = dalloc<int8_t>(std::max(nC, 1), st);
+    int32_t* ovf_list = dalloc<int32_t>(std::max(nC, 1), st);
+    AJ_CUDA(cudaMemsetAsync(row_ovf, 0, std::max(nC, 1), st));
+    int* ovf = counters + 5;   // [5] fallback rows, [6] error
+    AJ_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
     static bool attr_set = false;
     if (!attr_set) {
-      AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
-      AJ_CUDA(cudaFuncSetAttribute(k_schur<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
       attr_set = true;
     }
-    int* ovf = counters + 5;
-    AJ_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
-    k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
-                                                     b12, P.tau_drop, cand, cnt, nullptr, nullptr, ovf);
+    k_schur<false, false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
+                                                            partner, b11, b12, P.tau_drop, scr, cnt, nullptr,
+                                                            nullptr, row_ovf, ovf_list, ovf, ovf + 1);
     AJ_LAUNCHED();
-    const int o = read_scalar(ovf, st);
-    AJ_REQUIRE(o == 0, AJ_ERR_CAPACITY,
-               o == 1 ? "Schur complement: more than 96 pivot blocks adjacent to one row (raise tau_drop)"
-                      : "Schur complement: more than 3072 candidate columns in one row (raise tau_drop)");
+    int hov[2];
+    AJ_CUDA(cudaMemcpyAsync(hov, ovf, sizeof(hov), cudaMemcpyDeviceToHost, st));
+    AJ_CUDA(cudaStreamSynchronize(st));
+    const int nov = hov[0];
+    int32_t* scrg = nullptr;
+    if (nov > 0) {
+      scrg = dalloc<int32_t>((size_t)gsg * SW * schur_scratch_words<HTG, true>(), st);
+      k_schur<false, true><<<gsg, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
+                                                     b11, b12, P.tau_drop, scrg, cnt, nullptr, nullptr, row_ovf,
+                                                     ovf_list, ovf, ovf + 1);
+      AJ_LAUNCHED();
+      const int err = read_scalar(ovf + 1, st);
+      AJ_REQUIRE(err == 0, AJ_ERR_CAPACITY,
+                 err == 1 ? "Schur complement: more than 2048 pivot blocks adjacent to one row (raise tau_drop)"
+                          : "Schur complement: more than 24576 candidate columns in one row (raise tau_drop)");
+    }
     S.nnz = counts_to_ptr(cnt, S.ptr, nC, st);
     S.col = dalloc<int32_t>(S.nnz, st);
     S.val = dalloc<double>(S.nnz, st);
-    k_schur<true><<<gs, SW * 32, kSchurSmem, st>>>(nC, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
-                                                    b12, P.tau_drop, cand, S.ptr, S.col, S.val, ovf);
+    k_schur<true, false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
+                                                           partner, b11, b12, P.tau_drop, scr, S.ptr, S.col, S.val,
+                                                           row_ovf, ovf_list, ovf, ovf + 1);
     AJ_LAUNCHED();
-    dfree(cand, st);
+    if (nov > 0) {
+      k_schur<true, true><<<gsg, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
+                                                    b11, b12, P.tau_drop, scrg, S.ptr, S.col, S.val, row_ovf,
+                                                    ovf_list, ovf, ovf + 1);
+      AJ_LAUNCHED();
+      dfree(scrg, st);
+    }
+    lv.schur_fallback_rows = nov;
+    dfree(scr, st);
+    dfree(row_ovf, st);
+    dfree(ovf_list, st);
     dfree(cnt, st);
     lv.nnzS = S.nnz;
   }
@@ -1066,9 +1223,24 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   return true;
 }
 
+static void precond_capture(Precond* K, cudaStream_t st);
+
+static bool verbose_setup() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AJ_VERBOSE");
+    v = (e && atoi(e) > 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+static double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,
                         cudaStream_t st) {
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "precond_setup: L must be >= 3");
+  (void)num_sms();  // device init: SM count + memory-pool release threshold
   AJ_REQUIRE(P.kappa > 1.0 && P.tau_drop >= 0.0 && P.tau_strong >= 0.0 && P.cand_cap >= 64,
              AJ_ERR_ARG, "precond_setup: invalid parameters");
   const int64_t n64 = (int64_t)L * L * L;
@@ -1096,11 +1268,20 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       if (A.n <= P.n_coarse_max) break;
       Level lv;
       Csr S;
+      const double t0 = verbose_setup() ? wall_ms() : 0.0;
       if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
+      if (verbose_setup()) {
+        AJ_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[aj setup] level %d n=%d nF=%d pairs=%d mis_rounds=%d nnzA=%lld nnzS=%lld nnzL=%lld %.2f ms\n", lev,
+                lv.n, lv.nF, lv.npairs, lv.rounds, (long long)A.nnz, (long long)S.nnz, (long long)lv.nnzL,
+                wall_ms() - t0);
+      }
       if (lev > 0) {
         lv.r = dalloc<double>(lv.n, st);
         lv.z = dalloc<double>(lv.n, st);
       }
+      lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0);
+      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0);
       K->lv.push_back(lv);
       A.release(st);
       A = S;
@@ -1113,6 +1294,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
     K->rc = dalloc<double>(std::max(nc, 1), st);
     K->zc = dalloc<double>(std::max(nc, 1), st);
     K->G = dalloc<double>(std::max<int64_t>((int64_t)nc * nc, 1), st);
+    const double tc0 = verbose_setup() ? wall_ms() : 0.0;
     if (nc > 0) {
       double* M = dalloc<double>((int64_t)nc * 2 * nc, st);
       double* fcol = dalloc<double>(nc, st);
@@ -1135,6 +1317,10 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       dfree(M, st);
       dfree(fcol, st);
       dfree(sing, st);
+    }
+    if (verbose_setup()) {
+      AJ_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "[aj setup] coarse n=%d dense inverse %.2f ms\n", nc, wall_ms() - tc0);
     }
     A.release(st);
   } catch (...) {
@@ -1163,11 +1349,13 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   }
   I.setup_ms = ms;
   K->bytes_per_apply = precond_bytes_per_apply(K);
+  precond_capture(K, st);
   return K;
 }
 
 void precond_destroy(Precond* K, cudaStream_t st) {
   if (!K) return;
+  if (K->exec) cudaGraphExecDestroy(K->exec);
   for (auto& l : K->lv) l.release(st);
   dfree(K->G, st);
   dfree(K->rc, st);
@@ -1175,37 +1363,62 @@ void precond_destroy(Precond* K, cudaStream_t st) {
   delete K;
 }
 
+// levels >= 1 and the coarse solve, between internal buffers (captured once
+// into a CUDA graph at the end of precond_create)
+static void precond_inner(const Precond* K, cudaStream_t st) {
+  const int nl = (int)K->lv.size();
+  for (int l = 1; l < nl; ++l) {
+    const Level& v = K->lv[l];
+    launch_fwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].r : K->rc, st);
+  }
+  if (K->nc > 0) {
+    const double* rin = (nl >= 1) ? K->rc : nullptr;
+    if (nl >= 1) {
+      k_dense_mv<<<std::max(1, ceil_div((int64_t)K->nc * 32, TB)), TB, 0, st>>>(K->nc, K->G, rin, K->zc);
+      AJ_LAUNCHED();
+    }
+  }
+  for (int l = nl - 1; l >= 1; --l) {
+    const Level& v = K->lv[l];
+    launch_bwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].z : K->zc, v.z, st);
+  }
+}
+
+static void precond_capture(Precond* K, cudaStream_t st) {
+  if (K->lv.size() < 1) return;
+  cudaStream_t cs;
+  AJ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  AJ_CUDA(cudaStreamSynchronize(st));
+  const int64_t before = g_launches;
+  AJ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  precond_inner(K, cs);
+  cudaGraph_t g;
+  AJ_CUDA(cudaStreamEndCapture(cs, &g));
+  K->graph_nodes = g_launches - before;
+  g_launches = before;
+  AJ_CUDA(cudaGraphInstantiate(&K->exec, g, 0));
+  AJ_CUDA(cudaGraphDestroy(g));
+  AJ_CUDA(cudaStreamDestroy(cs));
+}
+
 // z = K^{-1} r
 void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st) {
   ProfScope ps(PROF_PREC, (double)K->bytes_per_apply, st);
   const int nl = (int)K->lv.size();
-  // forward sweep
-  const double* rin = r;
-  for (int l = 0; l < nl; ++l) {
-    const Level& v = K->lv[l];
-    double* rn = (l + 1 < nl) ? K->lv[l + 1].r : K->rc;
-    if (v.nC > 0) {
-      k_apply_fwd<<<grid_for(v.nC), TB, 0, st>>>(v.nC, v.cidx, v.D, rin, v.Lptr, v.Lcol, v.Lval, rn);
-      AJ_LAUNCHED();
-    }
-    rin = rn;
-  }
-  // coarse
-  if (K->nc > 0) {
-    double* zc = (nl == 0) ? z : K->zc;
-    k_dense_mv<<<std::max(1, ceil_div((int64_t)K->nc * 32, TB)), TB, 0, st>>>(K->nc, K->G, rin, zc);
+  if (nl == 0) {
+    k_dense_mv<<<std::max(1, ceil_div((int64_t)K->nc * 32, TB)), TB, 0, st>>>(K->nc, K->G, r, z);
     AJ_LAUNCHED();
+    return;
   }
-  // backward sweep
-  for (int l = nl - 1; l >= 0; --l) {
-    const Level& v = K->lv[l];
-    const double* rl = (l == 0) ? r : v.r;
-    double* zl = (l == 0) ? z : v.z;
-    const double* zn = (l + 1 < nl) ? K->lv[l + 1].z : K->zc;
-    k_apply_bwd<<<grid_for(v.n), TB, 0, st>>>(v.n, v.cmap, v.D, rl, v.partner, v.b11, v.b12, v.LTptr, v.LTcol,
-                                              v.LTval, zn, zl);
-    AJ_LAUNCHED();
+  const Level& v0 = K->lv[0];
+  launch_fwd(v0, r, (nl > 1) ? K->lv[1].r : K->rc, st);
+  if (K->exec) {
+    AJ_CUDA(cudaGraphLaunch(K->exec, st));
+    g_launches += K->graph_nodes;
+  } else {
+    precond_inner(K, st);
   }
+  launch_bwd(v0, r, (nl > 1) ? K->lv[1].z : K->zc, z, st);
 }
 
 int64_t precond_bytes_per_apply(const Precond* K) {

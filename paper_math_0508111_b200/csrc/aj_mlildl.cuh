@@ -16,20 +16,22 @@ struct Csr {
 };
 
 struct Level {
-  int n = 0, nF = 0, nC = 0, npairs = 0, rounds = 0;
+  int n = 0, nF = 0, nC = 0, npairs = 0, rounds = 0, schur_fallback_rows = 0;
   int64_t nnzL = 0, nnzLT = 0, nnzS = 0;
   double* D = nullptr;          // n   symmetric scaling of this level
   int32_t* cmap = nullptr;      // n   coarse index of C nodes, -1 for F
   int32_t* cidx = nullptr;      // nC  level index of coarse node c'
+  int32_t* fidx = nullptr;      // nF  level index of pivot node f'
   int32_t* partner = nullptr;   // n   2x2 partner of F nodes, else -1
   double* b11 = nullptr;        // n   B^{-1}[f,f]   (F nodes)
   double* b12 = nullptr;        // n   B^{-1}[f,g]   (F nodes of a pair)
   int64_t* Lptr = nullptr;      // nC+1
   int32_t* Lcol = nullptr;      // level index of F node
   double* Lval = nullptr;       // L_cf * D_f
-  int64_t* LTptr = nullptr;     // n+1 (F rows only non-empty)
+  int64_t* LTptr = nullptr;     // nF+1, rows in F order
   int32_t* LTcol = nullptr;     // coarse index
   double* LTval = nullptr;      // L_cf
+  int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;
   void release(cudaStream_t st);
@@ -45,6 +47,8 @@ struct Precond {
   double* zc = nullptr;
   aj_precond_info info{};
   int64_t bytes_per_apply = 0;
+  cudaGraphExec_t exec = nullptr;  // levels >= 1 + coarse, captured once
+  int64_t graph_nodes = 0;
 };
 
 Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,

@@ -74,15 +74,86 @@ __global__ void __launch_bounds__(SBX* SBY)
                                                        gridDim.x * gridDim.y * gridDim.z);
 }
 
+// Even-L variant: every lane owns two consecutive x-sites (16-byte loads and
+// stores of x, eps and y); the x-neighbours i-1 / i+2 come from the adjacent
+// lanes by warp shuffle, only tile-edge lanes touch memory for them.
+template <int NV>
+__global__ void __launch_bounds__(SBX* SBY)
+    k_spmv2(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
+            double hop, double sig, int kchunk, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
+  const int lane = threadIdx.x;
+  const int i = (blockIdx.x * SBX + lane) * 2;
+  const int j = blockIdx.y * SBY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, L);
+  const bool act = (i < L) && (j < L);
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+  const int64_t P = (int64_t)L * L;
+  const int jj = act ? j : 0, ii = act ? i : 0;
+  const int jm = (jj == 0) ? L - 1 : jj - 1, jp = (jj == L - 1) ? 0 : jj + 1;
+  const int64_t r0 = (int64_t)jj * L, rm = (int64_t)jm * L, rp = (int64_t)jp * L;
+  const int im = (ii == 0) ? L - 1 : ii - 1, ip2 = (ii + 2 >= L) ? ii + 2 - L : ii + 2;
+  const bool edge_l = (lane == 0), edge_r = (lane == SBX - 1) || (ii + 2 >= L);
+  if (k0 < L) {
+    const int km = (k0 == 0) ? L - 1 : k0 - 1;
+    double2 xm = make_double2(0.0, 0.0), xc = xm;
+    if (act) {
+      xm = __ldg(reinterpret_cast<const double2*>(&x[km * P + r0 + ii]));
+      xc = __ldg(reinterpret_cast<const double2*>(&x[(int64_t)k0 * P + r0 + ii]));
+    }
+    for (int k = k0; k < k1; ++k) {
+      const int kp = (k == L - 1) ? 0 : k + 1;
+      const int64_t b = (int64_t)k * P;
+      double2 xp = make_double2(0.0, 0.0), xr0 = xp, xr1 = xp, e2 = xp;
+      double left = 0.0, right = 0.0;
+      if (act) {
+        xp = __ldg(reinterpret_cast<const double2*>(&x[kp * P + r0 + ii]));
+        xr0 = __ldg(reinterpret_cast<const double2*>(&x[b + rm + ii]));
+        xr1 = __ldg(reinterpret_cast<const double2*>(&x[b + rp + ii]));
+        e2 = __ldg(reinterpret_cast<const double2*>(&eps[b + r0 + ii]));
+        if (edge_l) left = __ldg(&x[b + r0 + im]);
+        if (edge_r) right = __ldg(&x[b + r0 + ip2]);
+      }
+      const double sl = __shfl_up_sync(0xffffffffu, xc.y, 1);
+      const double sr = __shfl_down_sync(0xffffffffu, xc.x, 1);
+      if (!edge_l) left = sl;
+      if (!edge_r) right = sr;
+      double2 v;
+      const double s0 = (left + xc.y) + (xr0.x + xr1.x) + (xm.x + xp.x);
+      const double s1 = (xc.x + right) + (xr0.y + xr1.y) + (xm.y + xp.y);
+      v.x = hop * s0 + (e2.x - sig) * xc.x;
+      v.y = hop * s1 + (e2.y - sig) * xc.y;
+      if (act) {
+        *reinterpret_cast<double2*>(&y[b + r0 + ii]) = v;
+        if constexpr (NV > 0) {
+#pragma unroll
+          for (int c = 0; c < NV; ++c) {
+            const double2 w = __ldg(reinterpret_cast<const double2*>(&Wv[c * ld + b + r0 + ii]));
+            acc[c] += v.x * w.x + v.y * w.y;
+          }
+        }
+      }
+      xm = xc;
+      xc = xp;
+    }
+  }
+  if constexpr (NV > 0)
+    block_reduce_finalize<NV, SBX * SBY>(acc, rb, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                                         gridDim.x * gridDim.y * gridDim.z);
+}
+
 static dim3 spmv_grid(int L, int& kchunk) {
-  int tiles = ceil_div(L, SBX) * ceil_div(L, SBY);
+  const int tx = (L % 2 == 0) ? ceil_div(L, 2 * SBX) : ceil_div(L, SBX);
+  int tiles = tx * ceil_div(L, SBY);
   // aim for >= 4 waves of 256-thread CTAs over 148 SMs, chunks of >= 4 planes
   int want = num_sms() * 8;
   int nz = std::max(1, std::min(L, ceil_div(want, tiles)));
   kchunk = std::max(4, ceil_div(L, nz));
   kchunk = std::min(kchunk, L);
   nz = ceil_div(L, kchunk);
-  return dim3(ceil_div(L, SBX), ceil_div(L, SBY), nz);
+  return dim3(tx, ceil_div(L, SBY), nz);
 }
 
 int spmv_grid_blocks(int L) {
@@ -96,7 +167,10 @@ void launch_spmv(double* y, const double* x, const double* eps, int L, double ho
   int kc;
   dim3 g = spmv_grid(L, kc);
   ProfScope ps(PROF_SPMV, 24.0 * L * L * L, st);
-  k_spmv<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
+  if (L % 2 == 0)
+    k_spmv2<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
+  else
+    k_spmv<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
   AJ_LAUNCHED();
 }
 
@@ -107,8 +181,13 @@ void launch_spmv_dots(double* y, const double* x, const double* eps, int L, doub
   dim3 b(SBX, SBY);
   ProfScope ps(PROF_SPMV, (24.0 + 8.0 * nv) * L * L * L, st);
   switch (nv) {
-#define CASE(N) \
-  case N: k_spmv<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb); break;
+#define CASE(N)                                                               \
+  case N:                                                                     \
+    if (L % 2 == 0)                                                           \
+      k_spmv2<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);     \
+    else                                                                      \
+      k_spmv<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);      \
+    break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     default:

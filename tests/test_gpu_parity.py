@@ -276,3 +276,22 @@ def test_jd_host_e2e(gpu_lib):
     for i in range(5):
         r = an.stencil_apply(L, eps, Xh[i], hop=hop) - lam[i] * Xh[i]
         assert np.linalg.norm(r) <= 1e-8 * normA
+
+
+def test_precond_tail_paths_agree(gpu_lib, monkeypatch):
+    # the persistent cooperative apply (default) and the captured per-level graph
+    # (AJ_TAIL=0) implement the same operator
+    import torch
+    L = 24
+    eps = gpu_eps(gpu_lib, L, 16.5, 8)
+    r = T(rand_vec(L ** 3, 8))
+    K1 = gpu_lib.Precond(eps, L, -1.0, 0.0)
+    monkeypatch.setenv("AJ_TAIL", "0")
+    K2 = gpu_lib.Precond(eps, L, -1.0, 0.0)
+    z1, z2 = torch.empty_like(r), torch.empty_like(r)
+    K1.apply(z1, r)
+    K2.apply(z2, r)
+    assert K1.info()["levels"] >= 3
+    assert torch.linalg.norm(z1 - z2) <= 1e-12 * torch.linalg.norm(z1)
+    K1.free()
+    K2.free()

@@ -73,13 +73,16 @@ AJ_API int spmv(double* d_y, const double* d_x, const double* d_eps, int32_t L, 
  * ------------------------------------------------------------------------- */
 typedef struct {
   double kappa;          /* inverse bound, paper default 5    */
-  double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa)        */
-  double tau_strong;     /* strong-coupling threshold of the independent sets    */
+  double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa);
+                            < 0: auto, 2e-3 * min(1, (50/L)^2)                    */
+  double tau_strong;     /* strong-coupling threshold of the independent sets;
+                            < 0: auto, 10 * tau_drop                              */
   int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
-  int32_t max_levels;    /* level cap                                            */
+  int32_t max_levels;    /* level cap (<= 255)                                   */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
   int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN)      */
-  int32_t cand_cap;      /* per-row Schur candidate capacity (else CAPACITY)     */
+  int32_t cand_cap;      /* reserved (>= 64)                                     */
+  int32_t factor_fp32;   /* 1: store L / L^T values in fp32 (fp64 accumulation)  */
 } aj_precond_params;
 
 typedef struct {
@@ -92,6 +95,8 @@ typedef struct {
   int32_t level_pairs[256]; /* 2x2 pivots at each level                           */
   int64_t level_nnzS[256];  /* nnz of the Schur complement produced by each level */
   double setup_ms;        /* device time of precond_setup                         */
+  double tau_drop;        /* resolved drop tolerance                              */
+  double tau_strong;      /* resolved strong-coupling threshold                   */
 } aj_precond_info;
 
 AJ_API void aj_precond_default_params(aj_precond_params* p);

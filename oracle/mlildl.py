@@ -367,8 +367,12 @@ class MultilevelILDL:
     """M^{-1} ~ (A - sigma I)^{-1}; see module docstring."""
 
     def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
-                 n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192):
+                 n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False):
+        """factor_fp32 (reading R16): the stored factor values are rounded to
+        IEEE binary32 -- forward entries as fl32(l_cf * D_f), backward entries as
+        fl32(l_cf) -- and used in fp64 arithmetic, as on the GPU."""
         self.levels = []
+        self.factor_fp32 = bool(factor_fp32)
         cur = sp.csr_matrix(A)
         self.nnzA = cur.nnz
         for lev in range(max_levels):
@@ -378,6 +382,12 @@ class MultilevelILDL:
                               lattice_L if lev == 0 else None, stall_frac)
             if Lv is None:
                 break
+            if self.factor_fp32:
+                Lc = Lv.L.tocoo()
+                fw = (Lc.data * Lv.D[Lc.col]).astype(np.float32).astype(np.float64)
+                Lv.Lfwd = sp.csr_matrix((fw, (Lc.row, Lc.col)), shape=Lv.L.shape)
+                Lv.Lbwd = sp.csr_matrix((Lc.data.astype(np.float32).astype(np.float64), (Lc.row, Lc.col)),
+                                        shape=Lv.L.shape)
             self.levels.append(Lv)
             cur = Lv.S
         if cur.shape[0] > dense_cap:
@@ -403,10 +413,13 @@ class MultilevelILDL:
             return self.G @ r
         Lv = self.levels[lev]
         rh = Lv.D * r
-        wC = rh[Lv.C] - Lv.L @ rh
+        if self.factor_fp32:
+            wC = rh[Lv.C] - Lv.Lfwd @ r
+        else:
+            wC = rh[Lv.C] - Lv.L @ rh
         yC = self._apply(wC, lev + 1)
         zh = np.empty_like(r)
         zh[Lv.C] = yC
-        zF = Lv.Binv @ rh - Lv.L.T @ yC
+        zF = Lv.Binv @ rh - (Lv.Lbwd if self.factor_fp32 else Lv.L).T @ yC
         zh[Lv.F] = zF[Lv.F]
         return Lv.D * zh

@@ -81,13 +81,14 @@ int spmv(double* d_y, const double* d_x, const double* d_eps, int32_t L, double 
 void aj_precond_default_params(aj_precond_params* p) {
   if (!p) return;
   p->kappa = 5.0;
-  p->tau_drop = 2e-3;      // eps/kappa with eps = 1e-2 (R10)
-  p->tau_strong = 2e-2;    // 10 x tau_drop (R9)
+  p->tau_drop = -1.0;      // auto: 2e-3 (50/L)^2 (R12)
+  p->tau_strong = -1.0;    // auto: 10 x tau_drop
   p->n_coarse_max = 1024;
-  p->max_levels = 200;
+  p->max_levels = 255;
   p->stall_frac = 0.005;
   p->dense_cap = 4096;
   p->cand_cap = 2048;
+  p->factor_fp32 = 0;      // DESIGN.md R16: fp32 storage is opt-in (hurts at large L)
 }
 
 int precond_setup(void** handle, const double* d_eps, int32_t L, double hop, double sigma,

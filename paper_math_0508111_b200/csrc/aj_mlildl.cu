@@ -414,13 +414,13 @@ __global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __r
 }
 
 // L rows (coarse c'): entries (u, l_cu * D_u) with |l_cu| >= tau_drop
-template <bool FILL>
+template <bool FILL, typename TV>
 __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t* __restrict__ ptr,
                          const int32_t* __restrict__ col, const double* __restrict__ ah,
                          const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
                          const double* __restrict__ b11, const double* __restrict__ b12,
                          const double* __restrict__ D, double tau, int64_t* __restrict__ cnt_or_ptr,
-                         int32_t* __restrict__ Lcol, double* __restrict__ Lval) {
+                         int32_t* __restrict__ Lcol, TV* __restrict__ Lval) {
   for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
     const int c = cidx[cp];
     int64_t w = FILL ? cnt_or_ptr[cp] : 0;
@@ -429,14 +429,14 @@ __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t
                         if (fabs(lf) >= tau) {
                           if (FILL) {
                             Lcol[w] = f;
-                            Lval[w] = lf * D[f];
+                            Lval[w] = (TV)(lf * D[f]);
                           }
                           ++w;
                         }
                         if (g >= 0 && fabs(lg) >= tau) {
                           if (FILL) {
                             Lcol[w] = g;
-                            Lval[w] = lg * D[g];
+                            Lval[w] = (TV)(lg * D[g]);
                           }
                           ++w;
                         }
@@ -447,13 +447,13 @@ __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t
 
 // L^T rows (F index f' -> node u = fidx[f']): entries (cmap[c], l_cu) over C nodes c
 // adjacent to u or its partner
-template <bool FILL>
+template <bool FILL, typename TV>
 __global__ void k_LT_rows(int nF, const int32_t* __restrict__ fidx, const int64_t* __restrict__ ptr,
                           const int32_t* __restrict__ col, const double* __restrict__ ah,
                           const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
                           const double* __restrict__ b11, const double* __restrict__ b12,
                           const int32_t* __restrict__ cmap, double tau, int64_t* __restrict__ cnt_or_ptr,
-                          int32_t* __restrict__ LTcol, double* __restrict__ LTval) {
+                          int32_t* __restrict__ LTcol, TV* __restrict__ LTval) {
   for (int fp = blockIdx.x * TB + threadIdx.x; fp < nF; fp += gridDim.x * TB) {
     const int u = fidx[fp];
     int64_t w = FILL ? cnt_or_ptr[fp] : 0;
@@ -466,7 +466,7 @@ __global__ void k_LT_rows(int nF, const int32_t* __restrict__ fidx, const int64_
         if (fabs(l) >= tau) {
           if (FILL) {
             LTcol[w] = cmap[c];
-            LTval[w] = l;
+            LTval[w] = (TV)l;
           }
           ++w;
         }
@@ -487,7 +487,7 @@ __global__ void k_LT_rows(int nF, const int32_t* __restrict__ fidx, const int64_
         if (fabs(l) >= tau) {
           if (FILL) {
             LTcol[w] = cmap[c];
-            LTval[w] = l;
+            LTval[w] = (TV)l;
           }
           ++w;
         }
@@ -851,18 +851,18 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 // application kernels: G threads per row (G | 32), coalesced row segments,
 // shuffle reduction inside the group.  One row per group, no grid-stride
 // loop so every lane of a warp reaches the shuffles.
-template <int G>
+template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
     k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
                 const double* __restrict__ r, const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol,
-                const double* __restrict__ Lval, double* __restrict__ rn) {
+                const TV* __restrict__ Lval, double* __restrict__ rn) {
   const int gid = blockIdx.x * TB + threadIdx.x;
   const int cp = gid / G, lane = gid % G;
   const bool act = cp < nC;
   double acc = 0.0;
   if (act) {
     const int64_t e1 = Lptr[cp + 1];
-    for (int64_t e = Lptr[cp] + lane; e < e1; e += G) acc += Lval[e] * __ldg(&r[Lcol[e]]);
+    for (int64_t e = Lptr[cp] + lane; e < e1; e += G) acc += (double)Lval[e] * __ldg(&r[Lcol[e]]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -874,12 +874,12 @@ __global__ void __launch_bounds__(TB)
 
 // backward substitution: blocks [0, bF) take the pivot (F) rows with G lanes
 // each, blocks [bF, ...) copy the coarse solution back (z_c = D_c zn_c').
-template <int G>
+template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
     k_apply_bwd(int nF, int nC, int bF, const int32_t* __restrict__ fidx, const int32_t* __restrict__ cidx,
                 const double* __restrict__ D, const double* __restrict__ r, const int32_t* __restrict__ partner,
                 const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ LTptr,
-                const int32_t* __restrict__ LTcol, const double* __restrict__ LTval, const double* __restrict__ zn,
+                const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval, const double* __restrict__ zn,
                 double* __restrict__ z) {
   if ((int)blockIdx.x >= bF) {
     const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(TB)
   double acc = 0.0;
   if (act) {
     const int64_t e1 = LTptr[fp + 1];
-    for (int64_t e = LTptr[fp] + lane; e < e1; e += G) acc += LTval[e] * __ldg(&zn[LTcol[e]]);
+    for (int64_t e = LTptr[fp] + lane; e < e1; e += G) acc += (double)LTval[e] * __ldg(&zn[LTcol[e]]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -919,7 +919,13 @@ static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t
   const int G = v.gf;
   const int grid = std::max(1, ceil_div((int64_t)v.nC * G, TB));
   switch (G) {
-#define F(GG) case GG: k_apply_fwd<GG><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, v.Lval, rn); break;
+#define F(GG)                                                                                                 \
+  case GG:                                                                                                    \
+    if (v.f32)                                                                                                \
+      k_apply_fwd<GG, float><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, (const float*)v.Lval, rn); \
+    else                                                                                                      \
+      k_apply_fwd<GG, double><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, (const double*)v.Lval, rn); \
+    break;
     F(1) F(2) F(4) F(8) F(16) F(32)
 #undef F
   }
@@ -930,8 +936,15 @@ static void launch_bwd(const Level& v, const double* r, const double* zn, double
   const int bF = ceil_div((int64_t)v.nF * G, TB);
   const int grid = std::max(1, bF + ceil_div(v.nC, TB));
   switch (G) {
-#define B(GG) case GG: k_apply_bwd<GG><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11, \
-                                                         v.b12, v.LTptr, v.LTcol, v.LTval, zn, z); break;
+#define B(GG)                                                                                                  \
+  case GG:                                                                                                     \
+    if (v.f32)                                                                                                 \
+      k_apply_bwd<GG, float><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11, v.b12, \
+                                                  v.LTptr, v.LTcol, (const float*)v.LTval, zn, z);             \
+    else                                                                                                       \
+      k_apply_bwd<GG, double><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11,   \
+                                                   v.b12, v.LTptr, v.LTcol, (const double*)v.LTval, zn, z);    \
+    break;
     B(1) B(2) B(4) B(8) B(16) B(32)
 #undef B
   }
@@ -1133,14 +1146,19 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   {
     int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
     const int gc = grid_for(nC);
-    k_L_rows<false><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
+    k_L_rows<false, double><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
                                         P.tau_drop, cnt, nullptr, nullptr);
     AJ_LAUNCHED();
     lv.nnzL = counts_to_ptr(cnt, lv.Lptr, nC, st);
     lv.Lcol = dalloc<int32_t>(lv.nnzL, st);
-    lv.Lval = dalloc<double>(lv.nnzL, st);
-    k_L_rows<true><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
-                                       P.tau_drop, lv.Lptr, lv.Lcol, lv.Lval);
+    lv.f32 = P.factor_fp32 != 0;
+    lv.Lval = lv.f32 ? (void*)dalloc<float>(lv.nnzL, st) : (void*)dalloc<double>(lv.nnzL, st);
+    if (lv.f32)
+      k_L_rows<true, float><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D, P.tau_drop,
+                                                lv.Lptr, lv.Lcol, (float*)lv.Lval);
+    else
+      k_L_rows<true, double><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D, P.tau_drop,
+                                                 lv.Lptr, lv.Lcol, (double*)lv.Lval);
     AJ_LAUNCHED();
     dfree(cnt, st);
   }
@@ -1148,14 +1166,18 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   {
     int64_t* cnt = dalloc<int64_t>(nF, st);
     const int gF = grid_for(nF);
-    k_LT_rows<false><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
+    k_LT_rows<false, double><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
                                          P.tau_drop, cnt, nullptr, nullptr);
     AJ_LAUNCHED();
     lv.nnzLT = counts_to_ptr(cnt, lv.LTptr, nF, st);
     lv.LTcol = dalloc<int32_t>(lv.nnzLT, st);
-    lv.LTval = dalloc<double>(lv.nnzLT, st);
-    k_LT_rows<true><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
-                                        P.tau_drop, lv.LTptr, lv.LTcol, lv.LTval);
+    lv.LTval = lv.f32 ? (void*)dalloc<float>(lv.nnzLT, st) : (void*)dalloc<double>(lv.nnzLT, st);
+    if (lv.f32)
+      k_LT_rows<true, float><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
+                                                 P.tau_drop, lv.LTptr, lv.LTcol, (float*)lv.LTval);
+    else
+      k_LT_rows<true, double><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
+                                                  P.tau_drop, lv.LTptr, lv.LTcol, (double*)lv.LTval);
     AJ_LAUNCHED();
     dfree(cnt, st);
   }
@@ -1239,9 +1261,22 @@ static double wall_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,
+// Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 (50/L)^2, tau_strong =
+// 10 tau_drop (R12; the paper scales its drop tolerance with the size too,
+// eps = 1/sqrt(N)).
+aj_precond_params resolve_params(const aj_precond_params& in, int L) {
+  aj_precond_params P = in;
+  const double sc = (50.0 / L) * (50.0 / L);
+  if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
+  if (P.tau_strong < 0.0) P.tau_strong = 10.0 * P.tau_drop;
+  if (P.max_levels > 255) P.max_levels = 255;
+  return P;
+}
+
+Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& Pin,
                         cudaStream_t st) {
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "precond_setup: L must be >= 3");
+  const aj_precond_params P = resolve_params(Pin, L);
   (void)num_sms();  // device init: SM count + memory-pool release threshold
   AJ_REQUIRE(P.kappa > 1.0 && P.tau_drop >= 0.0 && P.tau_strong >= 0.0 && P.cand_cap >= 64,
              AJ_ERR_ARG, "precond_setup: invalid parameters");
@@ -1266,7 +1301,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
     k_lattice_csr<<<std::min(grid_for(n64), num_sms() * 16), TB, 0, st>>>(L, eps, hop, sigma, A.ptr, A.col,
                                                                            A.val);
     AJ_LAUNCHED();
-    for (int lev = 0; lev < P.max_levels && lev < 256; ++lev) {
+    for (int lev = 0; lev < P.max_levels && lev < 255; ++lev) {
       if (A.n <= P.n_coarse_max) break;
       Level lv;
       Csr S;
@@ -1350,6 +1385,8 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
     I.level_nnzS[l] = v.nnzS;
   }
   I.setup_ms = ms;
+  I.tau_drop = P.tau_drop;
+  I.tau_strong = P.tau_strong;
   K->bytes_per_apply = precond_bytes_per_apply(K);
   precond_capture(K, st);
   prepare_tail(K, st);
@@ -1506,8 +1543,12 @@ static void precond_inner(const Precond* K, cudaStream_t st) {
 
 static void prepare_tail(Precond* K, cudaStream_t st) {
   K->tail_grid = 0;
+  // opt-in (AJ_TAIL=1): measured slower than the captured per-level graph on B200
+  // (grid-wide barriers cost more than graph kernel boundaries: L=50 0.61 vs
+  // 0.36 ms, L=250 17.4 vs 7.2 ms per apply)
   const char* e = getenv("AJ_TAIL");
-  if (e && atoi(e) == 0) return;  // graph path forced
+  if (!(e && atoi(e) == 1)) return;
+  if (K->P.factor_fp32) return;  // the cooperative path reads fp64 factors only
   if (K->lv.size() < 2) return;
   std::vector<LevelDesc> h(K->lv.size());
   for (size_t l = 0; l < K->lv.size(); ++l) {
@@ -1515,7 +1556,8 @@ static void prepare_tail(Precond* K, cudaStream_t st) {
     LevelDesc& d = h[l];
     d.n = v.n; d.nF = v.nF; d.nC = v.nC; d.gf = v.gf; d.gb = v.gb;
     d.cidx = v.cidx; d.fidx = v.fidx; d.partner = v.partner; d.D = v.D; d.b11 = v.b11; d.b12 = v.b12;
-    d.Lptr = v.Lptr; d.LTptr = v.LTptr; d.Lcol = v.Lcol; d.LTcol = v.LTcol; d.Lval = v.Lval; d.LTval = v.LTval;
+    d.Lptr = v.Lptr; d.LTptr = v.LTptr; d.Lcol = v.Lcol; d.LTcol = v.LTcol;
+    d.Lval = (const double*)v.Lval; d.LTval = (const double*)v.LTval;
     d.r = v.r; d.z = v.z;
   }
   K->dlv = dalloc<LevelDesc>(h.size(), st);
@@ -1571,7 +1613,7 @@ int64_t precond_bytes_per_apply(const Precond* K) {
   // (8 B value + 4 B index) plus per-level vectors (r read twice, D, z/rn writes)
   int64_t b = 0;
   for (const auto& v : K->lv) {
-    b += (v.nnzL + v.nnzLT) * 12;
+    b += (v.nnzL + v.nnzLT) * (v.f32 ? 8 : 12);
     b += (int64_t)v.n * (8 /*D*/ + 8 /*r*/ + 8 /*z*/ + 4 /*cmap*/ + 8 * 2 /*b11,b12 for F*/ + 4 /*partner*/);
     b += (int64_t)v.nC * (4 + 8 + 8 + 8);  // cidx, D_c r_c, rn write, L ptr
   }

@@ -27,10 +27,11 @@ struct Level {
   double* b12 = nullptr;        // n   B^{-1}[f,g]   (F nodes of a pair)
   int64_t* Lptr = nullptr;      // nC+1
   int32_t* Lcol = nullptr;      // level index of F node
-  double* Lval = nullptr;       // L_cf * D_f
+  void* Lval = nullptr;         // L_cf * D_f  (float if f32, else double)
   int64_t* LTptr = nullptr;     // nF+1, rows in F order
   int32_t* LTcol = nullptr;     // coarse index
-  double* LTval = nullptr;      // L_cf
+  void* LTval = nullptr;        // L_cf        (float if f32, else double)
+  bool f32 = false;             // factor values stored in fp32 (accumulation stays fp64)
   int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;
@@ -64,6 +65,7 @@ struct Precond {
   int64_t graph_nodes = 0;
 };
 
+aj_precond_params resolve_params(const aj_precond_params& in, int L);
 Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& P,
                         cudaStream_t st);
 void precond_destroy(Precond* K, cudaStream_t st);

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(SBX* SBY)
 // stores of x, eps and y); the x-neighbours i-1 / i+2 come from the adjacent
 // lanes by warp shuffle, only tile-edge lanes touch memory for them.
 template <int NV>
-__global__ void __launch_bounds__(SBX* SBY)
+__global__ void __launch_bounds__(SBX* SBY, 4)
     k_spmv2(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
             double hop, double sig, int kchunk, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
   const int lane = threadIdx.x;
@@ -97,22 +97,31 @@ __global__ void __launch_bounds__(SBX* SBY)
   const int im = (ii == 0) ? L - 1 : ii - 1, ip2 = (ii + 2 >= L) ? ii + 2 - L : ii + 2;
   const bool edge_l = (lane == 0), edge_r = (lane == SBX - 1) || (ii + 2 >= L);
   if (k0 < L) {
+    // register queue of planes k-1, k, k+1 and the diagonal of plane k; the
+    // loads of plane k+2 and of eps(k+1) are issued one iteration ahead so two
+    // independent HBM streams are in flight per thread
     const int km = (k0 == 0) ? L - 1 : k0 - 1;
-    double2 xm = make_double2(0.0, 0.0), xc = xm;
+    const int kp0 = (k0 == L - 1) ? 0 : k0 + 1;
+    const double2 z2 = make_double2(0.0, 0.0);
+    double2 xm = z2, xc = z2, xp = z2, ec = z2;
     if (act) {
       xm = __ldg(reinterpret_cast<const double2*>(&x[km * P + r0 + ii]));
       xc = __ldg(reinterpret_cast<const double2*>(&x[(int64_t)k0 * P + r0 + ii]));
+      xp = __ldg(reinterpret_cast<const double2*>(&x[(int64_t)kp0 * P + r0 + ii]));
+      ec = __ldg(reinterpret_cast<const double2*>(&eps[(int64_t)k0 * P + r0 + ii]));
     }
     for (int k = k0; k < k1; ++k) {
-      const int kp = (k == L - 1) ? 0 : k + 1;
       const int64_t b = (int64_t)k * P;
-      double2 xp = make_double2(0.0, 0.0), xr0 = xp, xr1 = xp, e2 = xp;
+      double2 xpp = z2, en = z2, xr0 = z2, xr1 = z2;
       double left = 0.0, right = 0.0;
       if (act) {
-        xp = __ldg(reinterpret_cast<const double2*>(&x[kp * P + r0 + ii]));
+        if (k + 1 < k1) {
+          const int kpp = (k + 2 >= L) ? k + 2 - L : k + 2;
+          xpp = __ldg(reinterpret_cast<const double2*>(&x[(int64_t)kpp * P + r0 + ii]));
+          en = __ldg(reinterpret_cast<const double2*>(&eps[b + P + r0 + ii]));
+        }
         xr0 = __ldg(reinterpret_cast<const double2*>(&x[b + rm + ii]));
         xr1 = __ldg(reinterpret_cast<const double2*>(&x[b + rp + ii]));
-        e2 = __ldg(reinterpret_cast<const double2*>(&eps[b + r0 + ii]));
         if (edge_l) left = __ldg(&x[b + r0 + im]);
         if (edge_r) right = __ldg(&x[b + r0 + ip2]);
       }
@@ -123,10 +132,10 @@ __global__ void __launch_bounds__(SBX* SBY)
       double2 v;
       const double s0 = (left + xc.y) + (xr0.x + xr1.x) + (xm.x + xp.x);
       const double s1 = (xc.x + right) + (xr0.y + xr1.y) + (xm.y + xp.y);
-      v.x = hop * s0 + (e2.x - sig) * xc.x;
-      v.y = hop * s1 + (e2.y - sig) * xc.y;
+      v.x = hop * s0 + (ec.x - sig) * xc.x;
+      v.y = hop * s1 + (ec.y - sig) * xc.y;
       if (act) {
-        *reinterpret_cast<double2*>(&y[b + r0 + ii]) = v;
+        __stcs(reinterpret_cast<double2*>(&y[b + r0 + ii]), v);
         if constexpr (NV > 0) {
 #pragma unroll
           for (int c = 0; c < NV; ++c) {
@@ -137,6 +146,8 @@ __global__ void __launch_bounds__(SBX* SBY)
       }
       xm = xc;
       xc = xp;
+      xp = xpp;
+      ec = en;
     }
   }
   if constexpr (NV > 0)

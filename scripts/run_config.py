@@ -1,0 +1,47 @@
+"""Run jd_solve on a BASELINE config through the C ABI and print timings/stats.
+
+python scripts/run_config.py <config index> [W override] [seed override]
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from inputs import CONFIGS  # noqa: E402
+from paper_math_0508111_b200 import binding  # noqa: E402
+
+
+def main():
+    c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    cfg = dict(CONFIGS[c])
+    if len(sys.argv) > 2:
+        cfg["W"] = float(sys.argv[2])
+    if len(sys.argv) > 3:
+        cfg["seed"] = int(sys.argv[3])
+    if len(sys.argv) > 4:
+        cfg["L"] = int(sys.argv[4])
+    L = cfg["L"]
+    eps = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
+    jp = binding.default_jd_params(verbose=1, max_outer=int(os.environ.get("AJ_MAX_OUTER", "600")))
+    t0 = time.perf_counter()
+    lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], jparams=jp)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    normA = 6 * abs(cfg["hop"]) + float(eps.abs().max())
+    G = (X.T @ X).cpu().numpy()
+    out = dict(config=c, L=L, W=cfg["W"], seed=cfg["seed"], wall_s=dt, setup_ms=st["setup_ms"],
+               solve_ms=st["solve_ms"], outer=st["outer"], inner=st["inner_total"],
+               levels=st["precond"]["levels"], coarse=st["precond"]["coarse_n"],
+               tau_drop=st["precond"]["tau_drop"], tau_strong=st["precond"]["tau_strong"],
+               nnzL_per_site=st["precond"]["nnz_L"] / L ** 3, eigenvalues=[float(v) for v in lam],
+               resid_rel=[float(v) / normA for v in res], orth_err=float(np.abs(G - np.eye(len(lam))).max()))
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

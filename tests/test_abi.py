@@ -57,7 +57,7 @@ def test_no_cpu_fallback_without_device(lib):
 def test_default_params(lib):
     from paper_math_0508111_b200 import binding
     p = binding.default_precond_params()
-    assert p.kappa == 5.0 and p.tau_drop > 0 and p.tau_strong >= p.tau_drop
+    assert p.kappa == 5.0 and p.tau_drop < 0 and p.tau_strong < 0   # auto rule (R12)
     j = binding.default_jd_params()
     assert 1 <= j.jmin < j.jmax <= 48
 

@@ -79,22 +79,32 @@ def test_spmv_plane_wave_gpu(gpu_lib):
 
 
 # ---------------------------------------------------------------- preconditioner
+def resolved(p, L):
+    """DESIGN.md R12 auto rule for negative drop parameters."""
+    td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
+    ts = p.tau_strong if p.tau_strong >= 0 else 10 * td
+    return td, ts
+
+
 def _oracle_precond(L, eps, hop, sigma, p):
     A = an.matrix(L, eps, hop=hop, sigma=sigma)
-    return mlildl.MultilevelILDL(A, lattice_L=L, kappa=p.kappa, tau_drop=p.tau_drop, tau_strong=p.tau_strong,
+    td, ts = resolved(p, L)
+    return mlildl.MultilevelILDL(A, lattice_L=L, kappa=p.kappa, tau_drop=td, tau_strong=ts,
                                  n_coarse_max=p.n_coarse_max, max_levels=p.max_levels, stall_frac=p.stall_frac,
-                                 dense_cap=p.dense_cap)
+                                 dense_cap=p.dense_cap, factor_fp32=bool(p.factor_fp32))
 
 
+@pytest.mark.parametrize("fp32", [1, 0])
 @pytest.mark.parametrize("L,W,seed,hop,sigma", [(8, 16.5, 1, -1.0, 0.0), (12, 16.5, 2, -1.0, 0.0),
                                                 (16, 12.0, 3, 1.0, 0.25), (11, 21.0, 4, -1.0, 0.0),
                                                 (20, 16.5, 5, -1.0, 0.0)])
-def test_precond_parity(gpu_lib, L, W, seed, hop, sigma):
+def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32):
     import torch
-    p = gpu_lib.default_precond_params(n_coarse_max=200)
+    p = gpu_lib.default_precond_params(n_coarse_max=200, factor_fp32=fp32)
     eps_g = gpu_eps(gpu_lib, L, W, seed)
     K = gpu_lib.Precond(eps_g, L, hop, sigma, p)
     info = K.info()
+    assert (info["tau_drop"], info["tau_strong"]) == resolved(p, L)
     eps = an.disorder(L, W, seed)
     M = _oracle_precond(L, eps, hop, sigma, p)
     # identical multilevel structure (decisions taken on the same fp64 values)
@@ -117,7 +127,8 @@ def test_precond_exactness_limit_gpu(gpu_lib):
     # no dropping, no kappa bound, true independent sets -> K^{-1} = (A - sigma I)^{-1}
     import torch
     L = 6
-    p = gpu_lib.default_precond_params(kappa=1e300, tau_drop=0.0, tau_strong=0.0, n_coarse_max=10, stall_frac=0.0)
+    p = gpu_lib.default_precond_params(kappa=1e300, tau_drop=0.0, tau_strong=0.0, n_coarse_max=10, stall_frac=0.0,
+                                       factor_fp32=0)
     eps = gpu_eps(gpu_lib, L, 16.5, 1)
     K = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
     x = T(rand_vec(L ** 3, 3))
@@ -279,15 +290,16 @@ def test_jd_host_e2e(gpu_lib):
 
 
 def test_precond_tail_paths_agree(gpu_lib, monkeypatch):
-    # the persistent cooperative apply (default) and the captured per-level graph
-    # (AJ_TAIL=0) implement the same operator
+    # the captured per-level graph (default) and the persistent cooperative apply
+    # (AJ_TAIL=1) implement the same operator
     import torch
     L = 24
     eps = gpu_eps(gpu_lib, L, 16.5, 8)
     r = T(rand_vec(L ** 3, 8))
-    K1 = gpu_lib.Precond(eps, L, -1.0, 0.0)
-    monkeypatch.setenv("AJ_TAIL", "0")
-    K2 = gpu_lib.Precond(eps, L, -1.0, 0.0)
+    p = gpu_lib.default_precond_params(factor_fp32=0)  # the cooperative path reads fp64 factors
+    K1 = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
+    monkeypatch.setenv("AJ_TAIL", "1")
+    K2 = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
     z1, z2 = torch.empty_like(r), torch.empty_like(r)
     K1.apply(z1, r)
     K2.apply(z2, r)

@@ -146,3 +146,19 @@ def test_preconditioner_effectiveness():
     assert np.linalg.norm(A @ x - b) <= 1e-9 * np.linalg.norm(b)
     x0, it0, res0, _ = sqmr(lambda v: A @ v, lambda v: v, b, tol=1e-10, maxit=150)
     assert res0 > 1e-6
+
+
+def test_fp32_factor_storage_close_to_fp64():
+    # reading R16: rounding the stored factor to binary32 perturbs the operator
+    # by ~1e-7 relative and leaves the preconditioner effective
+    L = 10
+    A = an.matrix(L, an.disorder(L, 16.5, 2), hop=-1.0)
+    M64 = mlildl.MultilevelILDL(A, lattice_L=L, n_coarse_max=200)
+    M32 = mlildl.MultilevelILDL(A, lattice_L=L, n_coarse_max=200, factor_fp32=True)
+    r = np.random.default_rng(1).standard_normal(L ** 3)
+    z64, z32 = M64.apply(r), M32.apply(r)
+    assert np.linalg.norm(z32 - z64) <= 1e-5 * np.linalg.norm(z64)
+    assert np.linalg.norm(z32 - z64) > 0.0
+    b = np.random.default_rng(5).standard_normal(L ** 3)
+    x, it, res, _ = sqmr(lambda v: A @ v, M32.apply, b, tol=1e-10, maxit=150)
+    assert res <= 1e-10

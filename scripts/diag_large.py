@@ -41,6 +41,14 @@ def main():
                        (2.5e-4, 2.5e-3)]:
             sqmr_its(L, tau_drop=td, tau_strong=ts, factor_fp32=0)
         return
+    if mode == "grid2":
+        L = int(sys.argv[2])
+        for td, ts in [(5e-4, 1e-2), (5e-4, 2e-2), (2.5e-4, 1e-2), (2.5e-4, 2e-2), (1e-3, 2e-2)]:
+            try:
+                sqmr_its(L, tau_drop=td, tau_strong=ts, factor_fp32=0)
+            except Exception as ex:
+                print(L, td, ts, "failed", ex, flush=True)
+        return
     if mode == "sqmr":
         for L in [50, 64, 80, 100]:
             sqmr_its(L)

@@ -307,3 +307,24 @@ def test_precond_tail_paths_agree(gpu_lib, monkeypatch):
     assert torch.linalg.norm(z1 - z2) <= 1e-12 * torch.linalg.norm(z1)
     K1.free()
     K2.free()
+
+
+def test_jd_config2_l100_properties(gpu_lib):
+    # BASELINE configs[2] at full size (n = 10^6): properties that hold at any size --
+    # residuals recomputed with the oracle stencil, orthonormality, Rayleigh quotients,
+    # and the same 5 eigenvalues from two independent start vectors.
+    cfg = CONFIGS[2]
+    L, W, seed, hop, k = cfg["L"], cfg["W"], cfg["seed"], cfg["hop"], cfg["k"]
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    e = an.disorder(L, W, seed)
+    normA = 6 + np.abs(e).max()
+    lam1, X1, res1, st1 = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop)
+    Xh = N(X1)
+    for i in range(k):
+        ax = an.stencil_apply(L, e, Xh[:, i], hop=hop)
+        assert np.linalg.norm(ax - lam1[i] * Xh[:, i]) <= 1e-8 * normA
+        assert abs(Xh[:, i] @ ax - lam1[i]) <= 1e-10 * normA
+    assert np.abs(Xh.T @ Xh - np.eye(k)).max() <= 1e-8
+    jp = gpu_lib.default_jd_params(seed=12345)
+    lam2, X2, res2, st2 = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop, jparams=jp)
+    assert np.allclose(np.sort(lam1), np.sort(lam2), atol=1e-10 * normA)

@@ -34,6 +34,35 @@ namespace aj {
 constexpr int TB = 256;
 static int grid_for(int64_t n) { return std::max(1, ceil_div(n, TB)); }
 
+// ---- sub-warp row groups: SG lanes per CSR row (coalesced row segments) ------
+constexpr int SG = 8;
+__device__ __forceinline__ unsigned sg_mask() {
+  const int lane = threadIdx.x & 31;
+  return ((1u << SG) - 1u) << (lane & ~(SG - 1));
+}
+__device__ __forceinline__ double sg_max(double v, unsigned m) {
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(m, v, o));
+  return v;
+}
+__device__ __forceinline__ double sg_sum(double v, unsigned m) {
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+  return v;
+}
+__device__ __forceinline__ int sg_min_i(int v, unsigned m) {
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(m, v, o));
+  return v;
+}
+__device__ __forceinline__ int sg_or_i(int v, unsigned m) {
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(m, v, o);
+  return v;
+}
+static int grid_sg(int64_t rows) { return std::max(1, std::min(ceil_div(rows * SG, TB), num_sms() * 32)); }
+
+
 // ----------------------------------------------------------------------------
 // level-0 CSR of A - sigma I on the lattice (7 sorted entries per row)
 __global__ void k_lattice_csr(int L, const double* __restrict__ eps, double hop, double sigma,
@@ -72,10 +101,13 @@ __global__ void k_lattice_csr(int L, const double* __restrict__ eps, double hop,
 // (i) scaling D_i = 1/sqrt(max_j |a_ij|); scaled values a^_ij = a_ij * (D_i D_j)
 __global__ void k_rowmax_scale(int n, const int64_t* __restrict__ ptr, const double* __restrict__ val,
                                double* __restrict__ D) {
-  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
-    double m = 0.0;
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) m = fmax(m, fabs(val[e]));
-    D[i] = (m > 0.0) ? 1.0 / sqrt(m) : 1.0;
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned m = sg_mask();
+  for (int i = (blockIdx.x * TB + threadIdx.x) / SG; i < n; i += gridDim.x * (TB / SG)) {
+    double mx = 0.0;
+    for (int64_t e = ptr[i] + gl; e < ptr[i + 1]; e += SG) mx = fmax(mx, fabs(val[e]));
+    mx = sg_max(mx, m);
+    if (gl == 0) D[i] = (mx > 0.0) ? 1.0 / sqrt(mx) : 1.0;
   }
 }
 
@@ -87,11 +119,13 @@ __global__ void k_scaled_quality(int n, const int64_t* __restrict__ ptr, const i
                                  double* __restrict__ ah, double* __restrict__ dg,
                                  double* __restrict__ lmax1, double* __restrict__ d1,
                                  int32_t* __restrict__ prop, int8_t* __restrict__ ok1, double kappa) {
-  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned m = sg_mask();
+  for (int i = (blockIdx.x * TB + threadIdx.x) / SG; i < n; i += gridDim.x * (TB / SG)) {
     const double Di = D[i];
     double diag = 0.0, cm = 0.0, os = 0.0;
-    int32_t p = -1;
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+    int32_t p = INT32_MAX;
+    for (int64_t e = ptr[i] + gl; e < ptr[i + 1]; e += SG) {
       const int32_t j = col[e];
       const double v = val[e] * (Di * D[j]);
       ah[e] = v;
@@ -100,19 +134,33 @@ __global__ void k_scaled_quality(int n, const int64_t* __restrict__ ptr, const i
       } else {
         const double a = fabs(v);
         os += a;
-        if (a > cm) {
+        if (a > cm) {  // lane-local: first (smallest j) maximum
           cm = a;
           p = j;
         }
       }
     }
-    const double ad = fabs(diag);
-    dg[i] = diag;
-    const double l1 = (ad > 0.0) ? cm / ad : INFINITY;
-    lmax1[i] = l1;
-    d1[i] = (ad > 0.0) ? os / ad : INFINITY;
-    prop[i] = p;
-    ok1[i] = (l1 <= kappa - 1.0 && diag != 0.0) ? 1 : 0;
+    // group reduction: max |a| with the smallest column among ties
+#pragma unroll
+    for (int o = SG / 2; o > 0; o >>= 1) {
+      const double cm2 = __shfl_xor_sync(m, cm, o);
+      const int32_t p2 = __shfl_xor_sync(m, p, o);
+      if (cm2 > cm || (cm2 == cm && p2 < p)) {
+        cm = cm2;
+        p = p2;
+      }
+    }
+    os = sg_sum(os, m);
+    diag = sg_sum(diag, m);  // exactly one lane holds the diagonal, the others 0
+    if (gl == 0) {
+      const double ad = fabs(diag);
+      dg[i] = diag;
+      const double l1 = (ad > 0.0) ? cm / ad : INFINITY;
+      lmax1[i] = l1;
+      d1[i] = (ad > 0.0) ? os / ad : INFINITY;
+      prop[i] = (cm > 0.0 || p != INT32_MAX) ? (p == INT32_MAX ? -1 : p) : -1;
+      ok1[i] = (l1 <= kappa - 1.0 && diag != 0.0) ? 1 : 0;
+    }
   }
 }
 
@@ -241,18 +289,21 @@ __global__ void k_mis_nbmin(int n, const int64_t* __restrict__ ptr, const int32_
                             const double* __restrict__ ah, double tau_s, const int32_t* __restrict__ leader,
                             const int8_t* __restrict__ status, const int32_t* __restrict__ rank,
                             int32_t* __restrict__ nbmin) {
-  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned msk = sg_mask();
+  for (int i = (blockIdx.x * TB + threadIdx.x) / SG; i < n; i += gridDim.x * (TB / SG)) {
     const int32_t l = leader[i];
-    if (l < 0 || status[l] != 0) continue;
+    if (l < 0 || status[l] != 0) continue;  // uniform inside the group
     int32_t m = INT32_MAX;
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+    for (int64_t e = ptr[i] + gl; e < ptr[i + 1]; e += SG) {
       const int32_t j = col[e];
       if (j == i || !(fabs(ah[e]) >= tau_s)) continue;
       const int32_t lj = leader[j];
       if (lj < 0 || lj == l || status[lj] != 0) continue;
       m = min(m, rank[lj]);
     }
-    nbmin[i] = m;
+    m = sg_min_i(m, msk);
+    if (gl == 0) nbmin[i] = m;
   }
 }
 __global__ void k_mis_win(int n, const int32_t* __restrict__ leader, const int32_t* __restrict__ partner,
@@ -269,18 +320,20 @@ __global__ void k_mis_remove(int n, const int64_t* __restrict__ ptr, const int32
                              const double* __restrict__ ah, double tau_s, const int32_t* __restrict__ leader,
                              const int8_t* __restrict__ status, const int8_t* __restrict__ win,
                              int8_t* __restrict__ rem) {
-  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned msk = sg_mask();
+  for (int i = (blockIdx.x * TB + threadIdx.x) / SG; i < n; i += gridDim.x * (TB / SG)) {
     const int32_t l = leader[i];
-    if (l < 0 || status[l] != 0 || win[l]) continue;
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+    if (l < 0 || status[l] != 0 || win[l]) continue;  // uniform inside the group
+    int hit = 0;
+    for (int64_t e = ptr[i] + gl; e < ptr[i + 1] && !hit; e += SG) {
       const int32_t j = col[e];
       if (j == i || !(fabs(ah[e]) >= tau_s)) continue;
       const int32_t lj = leader[j];
-      if (lj >= 0 && lj != l && win[lj]) {
-        rem[l] = 1;
-        break;
-      }
+      if (lj >= 0 && lj != l && win[lj]) hit = 1;
     }
+    hit = sg_or_i(hit, msk);
+    if (hit && gl == 0) rem[l] = 1;
   }
 }
 __global__ void k_mis_apply(int n, const int32_t* __restrict__ leader, int8_t* __restrict__ status,
@@ -317,9 +370,10 @@ __device__ __forceinline__ void for_blocks_of_row(int c, const int64_t* __restri
                                                   const int8_t* __restrict__ inF,
                                                   const int32_t* __restrict__ partner,
                                                   const double* __restrict__ b11,
-                                                  const double* __restrict__ b12, Fn fn) {
+                                                  const double* __restrict__ b12, Fn fn, int start = 0,
+                                                  int stride = 1) {
   const int64_t lo = ptr[c], hi = ptr[c + 1];
-  for (int64_t e = lo; e < hi; ++e) {
+  for (int64_t e = lo + start; e < hi; e += stride) {
     const int32_t u = col[e];
     if (u == c || !inF[u]) continue;
     const int32_t p = partner[u];
@@ -348,20 +402,34 @@ __global__ void k_budget(int n, const int64_t* __restrict__ ptr, const int32_t* 
                          const int32_t* __restrict__ partner, const double* __restrict__ b11,
                          const double* __restrict__ b12, double kappa, int8_t* __restrict__ nominate,
                          int* __restrict__ nviol) {
-  for (int c = blockIdx.x * TB + threadIdx.x; c < n; c += gridDim.x * TB) {
-    if (inF[c]) continue;
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned msk = sg_mask();
+  for (int c = (blockIdx.x * TB + threadIdx.x) / SG; c < n; c += gridDim.x * (TB / SG)) {
+    if (inF[c]) continue;  // uniform inside the group
     double budget = 0.0, wbest = -1.0;
     int32_t lbest = INT32_MAX;
-    for_blocks_of_row(c, ptr, col, ah, inF, partner, b11, b12,
-                      [&](int32_t f, int32_t g, double lf, double lg, int32_t lead) {
-                        const double w = fabs(lf) + (g >= 0 ? fabs(lg) : 0.0);
-                        budget += w;
-                        if (w > wbest || (w == wbest && lead < lbest)) {
-                          wbest = w;
-                          lbest = lead;
-                        }
-                      });
-    if (budget > kappa - 1.0) {
+    for_blocks_of_row(
+        c, ptr, col, ah, inF, partner, b11, b12,
+        [&](int32_t f, int32_t g, double lf, double lg, int32_t lead) {
+          const double w = fabs(lf) + (g >= 0 ? fabs(lg) : 0.0);
+          budget += w;
+          if (w > wbest || (w == wbest && lead < lbest)) {
+            wbest = w;
+            lbest = lead;
+          }
+        },
+        gl, SG);
+    budget = sg_sum(budget, msk);
+#pragma unroll
+    for (int o = SG / 2; o > 0; o >>= 1) {
+      const double w2 = __shfl_xor_sync(msk, wbest, o);
+      const int32_t l2 = __shfl_xor_sync(msk, lbest, o);
+      if (w2 > wbest || (w2 == wbest && l2 < lbest)) {
+        wbest = w2;
+        lbest = l2;
+      }
+    }
+    if (gl == 0 && budget > kappa - 1.0) {
       nominate[lbest] = 1;
       atomicAdd(nviol, 1);
     }
@@ -413,7 +481,8 @@ __global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __r
   }
 }
 
-// L rows (coarse c'): entries (u, l_cu * D_u) with |l_cu| >= tau_drop
+// L rows (coarse c'): entries (u, l_cu * D_u) with |l_cu| >= tau_drop; SG lanes per row,
+// each lane writes its own entries after a group prefix sum of the lane counts
 template <bool FILL, typename TV>
 __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t* __restrict__ ptr,
                          const int32_t* __restrict__ col, const double* __restrict__ ah,
@@ -421,27 +490,45 @@ __global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t
                          const double* __restrict__ b11, const double* __restrict__ b12,
                          const double* __restrict__ D, double tau, int64_t* __restrict__ cnt_or_ptr,
                          int32_t* __restrict__ Lcol, TV* __restrict__ Lval) {
-  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
+  const int gl = threadIdx.x & (SG - 1);
+  const unsigned msk = sg_mask();
+  for (int cp = (blockIdx.x * TB + threadIdx.x) / SG; cp < nC; cp += gridDim.x * (TB / SG)) {
     const int c = cidx[cp];
-    int64_t w = FILL ? cnt_or_ptr[cp] : 0;
-    for_blocks_of_row(c, ptr, col, ah, inF, partner, b11, b12,
-                      [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
-                        if (fabs(lf) >= tau) {
-                          if (FILL) {
-                            Lcol[w] = f;
-                            Lval[w] = (TV)(lf * D[f]);
-                          }
-                          ++w;
-                        }
-                        if (g >= 0 && fabs(lg) >= tau) {
-                          if (FILL) {
-                            Lcol[w] = g;
-                            Lval[w] = (TV)(lg * D[g]);
-                          }
-                          ++w;
-                        }
-                      });
-    if (!FILL) cnt_or_ptr[cp] = w;
+    int cnt = 0;
+    for_blocks_of_row(
+        c, ptr, col, ah, inF, partner, b11, b12,
+        [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
+          cnt += (fabs(lf) >= tau) + (g >= 0 && fabs(lg) >= tau);
+        },
+        gl, SG);
+    // inclusive scan of the lane counts inside the group
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < SG; o <<= 1) {
+      const int t = __shfl_up_sync(msk, incl, o, SG);
+      if (gl >= o) incl += t;
+    }
+    if (!FILL) {
+      const int tot = __shfl_sync(msk, incl, SG - 1, SG);
+      if (gl == 0) cnt_or_ptr[cp] = tot;
+      continue;
+    }
+    int64_t w = cnt_or_ptr[cp] + (incl - cnt);
+    for_blocks_of_row(
+        c, ptr, col, ah, inF, partner, b11, b12,
+        [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
+          if (fabs(lf) >= tau) {
+            Lcol[w] = f;
+            Lval[w] = (TV)(lf * D[f]);
+            ++w;
+          }
+          if (g >= 0 && fabs(lg) >= tau) {
+            Lcol[w] = g;
+            Lval[w] = (TV)(lg * D[g]);
+            ++w;
+          }
+        },
+        gl, SG);
   }
 }
 
@@ -1032,9 +1119,10 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   AJ_CUDA(cudaMemsetAsync(b12, 0, n * sizeof(double), st));
   AJ_CUDA(cudaMemsetAsync(nominate, 0, n, st));
 
-  k_rowmax_scale<<<g, TB, 0, st>>>(n, A.ptr, A.val, D);
+  const int gsg = grid_sg(n);
+  k_rowmax_scale<<<gsg, TB, 0, st>>>(n, A.ptr, A.val, D);
   AJ_LAUNCHED();
-  k_scaled_quality<<<g, TB, 0, st>>>(n, A.ptr, A.col, A.val, D, ah, dg, lmax1, d1, prop, ok1, P.kappa);
+  k_scaled_quality<<<gsg, TB, 0, st>>>(n, A.ptr, A.col, A.val, D, ah, dg, lmax1, d1, prop, ok1, P.kappa);
   AJ_LAUNCHED();
   if (latticeL == 0) {
     k_pairs<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, dg, d1, prop, ok1, P.kappa, partner, b11, b12, q,
@@ -1071,11 +1159,11 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     for (;;) {
       ++rounds;
       AJ_CUDA(cudaMemsetAsync(counters + 1, 0, sizeof(int), st));
-      k_mis_nbmin<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, rank, nbmin);
+      k_mis_nbmin<<<gsg, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, rank, nbmin);
       AJ_LAUNCHED();
       k_mis_win<<<g, TB, 0, st>>>(n, leader, partner, status, rank, nbmin, win);
       AJ_LAUNCHED();
-      k_mis_remove<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, win, rem);
+      k_mis_remove<<<gsg, TB, 0, st>>>(n, A.ptr, A.col, ah, P.tau_strong, leader, status, win, rem);
       AJ_LAUNCHED();
       k_mis_apply<<<g, TB, 0, st>>>(n, leader, status, win, rem, counters + 1);
       AJ_LAUNCHED();
@@ -1091,7 +1179,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   // row-budget repair (inverse-based bound on the rows of L^{-1})
   for (int it = 0;; ++it) {
     AJ_CUDA(cudaMemsetAsync(counters + 2, 0, sizeof(int), st));
-    k_budget<<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, P.kappa, nominate, counters + 2);
+    k_budget<<<gsg, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, b12, P.kappa, nominate, counters + 2);
     AJ_LAUNCHED();
     if (read_scalar(counters + 2, st) == 0) break;
     k_budget_apply<<<g, TB, 0, st>>>(n, partner, inF, nominate);
@@ -1145,7 +1233,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   // L (forward) rows over coarse nodes
   {
     int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
-    const int gc = grid_for(nC);
+    const int gc = grid_sg(nC);
     k_L_rows<false, double><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
                                         P.tau_drop, cnt, nullptr, nullptr);
     AJ_LAUNCHED();

@@ -658,15 +658,16 @@ __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int
 // GLOBAL = false: tables in shared memory (T = 2048); rows that do not fit are
 // flagged in row_ovf and queued in ovf_list.  GLOBAL = true: the fallback over
 // ovf_list with T = 32768 tables in global memory.
-template <bool FILL, bool GLOBAL>
+template <bool GLOBAL>
 __global__ void __launch_bounds__(SW * 32)
     k_schur(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
             const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
             const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
             const double* __restrict__ b11, const double* __restrict__ b12, double tau,
-            int32_t* __restrict__ scratch_all, int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ Scol,
-            double* __restrict__ Sval, int8_t* __restrict__ row_ovf, int32_t* __restrict__ ovf_list,
-            int* __restrict__ ovf_count, int* __restrict__ error) {
+            int32_t* __restrict__ scratch_all, int64_t* __restrict__ row_cnt, int64_t* __restrict__ row_off,
+            int32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, int64_t cap,
+            unsigned long long* __restrict__ cursor, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
+            int* __restrict__ error) {
   constexpr int T = GLOBAL ? HTG : HT;
   constexpr int BM = GLOBAL ? BMAXG : BMAX;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -692,7 +693,6 @@ __global__ void __launch_bounds__(SW * 32)
   __syncwarp();
   for (int ri = blockIdx.x * SW + wid; ri < nrows; ri += gridDim.x * SW) {
     const int cp = rowlist ? rowlist[ri] : ri;
-    if (!GLOBAL && FILL && row_ovf[cp]) continue;  // done by the fallback
     const int c = cidx[cp];
     const int64_t lo = ptr[c], hi = ptr[c + 1];
     __syncwarp();
@@ -802,58 +802,78 @@ __global__ void __launch_bounds__(SW * 32)
     }
     const int nc = min(scount[wid], T);
     const bool bad = (nb > BM) || __any_sync(0xffffffffu, full) || scount[wid] > (T * 3) / 4;
-    // (3) collect (key, value) through the slot list and reset those slots
-    int32_t* keys = list;
-    for (int t = lane; t < nc; t += 32) {
-      const int32_t sl = list[t];
-      const int32_t kk = tab[sl];
-      kvals[t] = vals[sl];
-      tab[sl] = -1;
-      keys[t] = kk;
-    }
-    __syncwarp();
-    if (bad) {
-      if (GLOBAL) {
-        if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
-      } else if (!FILL && lane == 0) {
-        row_ovf[cp] = 1;
-        ovf_list[atomicAdd(ovf_count, 1)] = cp;
-        cnt_or_ptr[cp] = 0;
-      }
-      continue;
-    }
-    int P = 1;
-    while (P < nc) P <<= 1;
-    for (int t = lane; t < P; t += 32) {  // sort in the (now empty) table storage
-      tab[t] = (t < nc) ? keys[t] : INT32_MAX;
-      vals[t] = (t < nc) ? kvals[t] : 0.0;
-    }
-    __syncwarp();
-    warp_bitonic_sort_kv(tab, vals, P);
-    const int64_t wbase = FILL ? cnt_or_ptr[cp] : 0;
+    // (3) collect (key, value) through the slot list, reset the slots, drop, and
+    //     compact the survivors (only those are sorted)
+    int32_t* keys = list;  // aliases the slot list: writes trail the reads
     int kept = 0;
     for (int t0 = 0; t0 < nc; t0 += 32) {
       const int t = t0 + lane;
       bool keep = false;
-      int32_t c2p = INT32_MAX;
-      double sv = 0.0;
+      int32_t kk = 0;
+      double vv = 0.0;
       if (t < nc) {
-        c2p = tab[t];
-        sv = vals[t];
-        keep = (c2p == cp) || (fabs(sv) >= tau);
+        const int32_t sl = list[t];
+        kk = tab[sl];
+        vv = vals[sl];
+        tab[sl] = -1;
+        keep = (kk == cp) || (fabs(vv) >= tau);
       }
+      __syncwarp();
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (FILL && keep) {
-        const int off = __popc(bal & ((1u << lane) - 1u));
-        Scol[wbase + kept + off] = c2p;
-        Sval[wbase + kept + off] = sv;
+      if (keep) {
+        const int off = kept + __popc(bal & ((1u << lane) - 1u));
+        keys[off] = kk;
+        kvals[off] = vv;
       }
       kept += __popc(bal);
+      __syncwarp();
     }
-    if (!FILL && lane == 0) cnt_or_ptr[cp] = kept;
+    if (bad) {
+      if (GLOBAL) {
+        if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
+      } else if (lane == 0) {
+        ovf_list[atomicAdd(ovf_count, 1)] = cp;
+      }
+      continue;
+    }
+    int P = 1;
+    while (P < kept) P <<= 1;
+    for (int t = lane; t < P; t += 32) {  // sort the survivors in the (now empty) table storage
+      tab[t] = (t < kept) ? keys[t] : INT32_MAX;
+      vals[t] = (t < kept) ? kvals[t] : 0.0;
+    }
+    __syncwarp();
+    warp_bitonic_sort_kv(tab, vals, P);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)kept);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane == 0) {
+      row_cnt[cp] = kept;
+      row_off[cp] = (int64_t)base;
+    }
+    if ((int64_t)base + kept <= cap) {
+      for (int t = lane; t < kept; t += 32) {
+        tmp_col[base + t] = tab[t];
+        tmp_val[base + t] = vals[t];
+      }
+    }
     __syncwarp();
     for (int t = lane; t < P; t += 32) tab[t] = -1;  // the table is empty again
     __syncwarp();
+  }
+}
+
+// gather the per-row runs of the one-pass Schur output into CSR order
+__global__ void k_schur_gather(int nC, const int64_t* __restrict__ Sptr, const int64_t* __restrict__ row_off,
+                               const int32_t* __restrict__ tmp_col, const double* __restrict__ tmp_val,
+                               int32_t* __restrict__ Scol, double* __restrict__ Sval) {
+  const int lane = threadIdx.x & 31;
+  for (int cp = (blockIdx.x * TB + threadIdx.x) >> 5; cp < nC; cp += (gridDim.x * TB) >> 5) {
+    const int64_t d0 = Sptr[cp], cnt = Sptr[cp + 1] - d0, s0 = row_off[cp];
+    for (int64_t t = lane; t < cnt; t += 32) {
+      Scol[d0 + t] = tmp_col[s0 + t];
+      Sval[d0 + t] = tmp_val[s0 + t];
+    }
   }
 }
 
@@ -1269,64 +1289,72 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     AJ_LAUNCHED();
     dfree(cnt, st);
   }
-  // Schur complement on the coarse nodes
+  // Schur complement on the coarse nodes: one pass, survivors appended to a temp
+  // buffer through a global cursor, then gathered into CSR order
   {
     S.n = nC;
-    int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
     const int nwarps_total = std::min(std::max(nC, 1), num_sms() * 8 * SW);
     const int gs = std::max(1, ceil_div(nwarps_total, SW));
-    const int gsg = std::min(gs, num_sms());  // fallback grid (large global tables)
+    const int gsg2 = std::min(gs, num_sms());  // fallback grid (large global tables)
     int32_t* scr = dalloc<int32_t>((size_t)gs * SW * schur_scratch_words<HT, false>(), st);
-    int8_t* row_ovf = dalloc<int8_t>(std::max(nC, 1), st);
+    int64_t* row_cnt = dalloc<int64_t>(std::max(nC, 1), st);
+    int64_t* row_off = dalloc<int64_t>(std::max(nC, 1), st);
     int32_t* ovf_list = dalloc<int32_t>(std::max(nC, 1), st);
-    AJ_CUDA(cudaMemsetAsync(row_ovf, 0, std::max(nC, 1), st));
+    unsigned long long* cursor = dalloc<unsigned long long>(1, st);
     int* ovf = counters + 5;   // [5] fallback rows, [6] error
-    AJ_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
     static bool attr_set = false;
     if (!attr_set) {
-      AJ_CUDA(cudaFuncSetAttribute(k_schur<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
-      AJ_CUDA(cudaFuncSetAttribute(k_schur<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
       attr_set = true;
     }
-    k_schur<false, false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
-                                                            partner, b11, b12, P.tau_drop, scr, cnt, nullptr,
-                                                            nullptr, row_ovf, ovf_list, ovf, ovf + 1);
-    AJ_LAUNCHED();
-    int hov[2];
-    AJ_CUDA(cudaMemcpyAsync(hov, ovf, sizeof(hov), cudaMemcpyDeviceToHost, st));
-    AJ_CUDA(cudaStreamSynchronize(st));
-    const int nov = hov[0];
+    int64_t cap = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
+    int nov = 0;
+    int32_t* tmp_col = nullptr;
+    double* tmp_val = nullptr;
     int32_t* scrg = nullptr;
-    if (nov > 0) {
-      scrg = dalloc<int32_t>((size_t)gsg * SW * schur_scratch_words<HTG, true>(), st);
-      k_schur<false, true><<<gsg, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
-                                                     b11, b12, P.tau_drop, scrg, cnt, nullptr, nullptr, row_ovf,
-                                                     ovf_list, ovf, ovf + 1);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      tmp_col = dalloc<int32_t>(cap, st);
+      tmp_val = dalloc<double>(cap, st);
+      AJ_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+      AJ_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+      k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
+                                                       b11, b12, P.tau_drop, scr, row_cnt, row_off, tmp_col, tmp_val,
+                                                       cap, cursor, ovf_list, ovf, ovf + 1);
       AJ_LAUNCHED();
-      const int err = read_scalar(ovf + 1, st);
-      AJ_REQUIRE(err == 0, AJ_ERR_CAPACITY,
-                 err == 1 ? "Schur complement: more than 2048 pivot blocks adjacent to one row (raise tau_drop)"
-                          : "Schur complement: more than 24576 candidate columns in one row (raise tau_drop)");
+      nov = read_scalar(ovf, st);
+      if (nov > 0) {
+        if (!scrg) scrg = dalloc<int32_t>((size_t)gsg2 * SW * schur_scratch_words<HTG, true>(), st);
+        k_schur<true><<<gsg2, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
+                                                 b12, P.tau_drop, scrg, row_cnt, row_off, tmp_col, tmp_val, cap,
+                                                 cursor, ovf_list, ovf, ovf + 1);
+        AJ_LAUNCHED();
+        const int err = read_scalar(ovf + 1, st);
+        AJ_REQUIRE(err == 0, AJ_ERR_CAPACITY,
+                   err == 1 ? "Schur complement: more than 2048 pivot blocks adjacent to one row (raise tau_drop)"
+                            : "Schur complement: more than 24576 candidate columns in one row (raise tau_drop)");
+      }
+      const int64_t used = (int64_t)read_scalar(cursor, st);
+      if (used <= cap) break;
+      dfree(tmp_col, st);
+      dfree(tmp_val, st);
+      cap = used;  // exact size now known: run again
+      AJ_REQUIRE(attempt == 0, AJ_ERR_CAPACITY, "Schur complement: temp capacity");
     }
-    S.nnz = counts_to_ptr(cnt, S.ptr, nC, st);
+    S.nnz = counts_to_ptr(row_cnt, S.ptr, nC, st);
     S.col = dalloc<int32_t>(S.nnz, st);
     S.val = dalloc<double>(S.nnz, st);
-    k_schur<true, false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
-                                                           partner, b11, b12, P.tau_drop, scr, S.ptr, S.col, S.val,
-                                                           row_ovf, ovf_list, ovf, ovf + 1);
+    k_schur_gather<<<std::max(1, std::min(ceil_div((int64_t)nC * 32, TB), num_sms() * 32)), TB, 0, st>>>(
+        nC, S.ptr, row_off, tmp_col, tmp_val, S.col, S.val);
     AJ_LAUNCHED();
-    if (nov > 0) {
-      k_schur<true, true><<<gsg, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
-                                                    b11, b12, P.tau_drop, scrg, S.ptr, S.col, S.val, row_ovf,
-                                                    ovf_list, ovf, ovf + 1);
-      AJ_LAUNCHED();
-      dfree(scrg, st);
-    }
+    if (scrg) dfree(scrg, st);
+    dfree(tmp_col, st);
+    dfree(tmp_val, st);
+    dfree(cursor, st);
+    dfree(row_off, st);
     lv.schur_fallback_rows = nov;
     dfree(scr, st);
-    dfree(row_ovf, st);
     dfree(ovf_list, st);
-    dfree(cnt, st);
+    dfree(row_cnt, st);
     lv.nnzS = S.nnz;
   }
   dfree(partner, st);

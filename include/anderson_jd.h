@@ -76,9 +76,9 @@ typedef struct {
   double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa);
                             < 0: auto, 2e-3 * min(1, (50/L)^2)                    */
   double tau_strong;     /* strong-coupling threshold of the independent sets;
-                            < 0: auto, 10 * tau_drop                              */
+                            < 0: auto, max(10 * tau_drop, 5e-3)                   */
   int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
-  int32_t max_levels;    /* level cap (<= 255)                                   */
+  int32_t max_levels;    /* level cap (<= 1023)                                  */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
   int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN)      */
   int32_t cand_cap;      /* reserved (>= 64)                                     */
@@ -90,10 +90,10 @@ typedef struct {
   int32_t coarse_n;       /* size of the dense coarse system                      */
   int64_t nnz_L;          /* stored entries of all L factors                      */
   int64_t nnz_A;          /* 7 n                                                  */
-  int32_t level_n[256];   /* size of each level                                   */
-  int32_t level_nF[256];  /* pivots eliminated at each level                      */
-  int32_t level_pairs[256]; /* 2x2 pivots at each level                           */
-  int64_t level_nnzS[256];  /* nnz of the Schur complement produced by each level */
+  int32_t level_n[1024];  /* size of each level                                   */
+  int32_t level_nF[1024]; /* pivots eliminated at each level                      */
+  int32_t level_pairs[1024]; /* 2x2 pivots at each level                          */
+  int64_t level_nnzS[1024];  /* nnz of the Schur complement produced by each level */
   double setup_ms;        /* device time of precond_setup                         */
   double tau_drop;        /* resolved drop tolerance                              */
   double tau_strong;      /* resolved strong-coupling threshold                   */

@@ -36,8 +36,8 @@ class PrecondParams(ctypes.Structure):
 
 class PrecondInfo(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("coarse_n", ctypes.c_int32), ("nnz_L", ctypes.c_int64),
-                ("nnz_A", ctypes.c_int64), ("level_n", ctypes.c_int32 * 256), ("level_nF", ctypes.c_int32 * 256),
-                ("level_pairs", ctypes.c_int32 * 256), ("level_nnzS", ctypes.c_int64 * 256),
+                ("nnz_A", ctypes.c_int64), ("level_n", ctypes.c_int32 * 1024), ("level_nF", ctypes.c_int32 * 1024),
+                ("level_pairs", ctypes.c_int32 * 1024), ("level_nnzS", ctypes.c_int64 * 1024),
                 ("setup_ms", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double)]
 
     def as_dict(self):

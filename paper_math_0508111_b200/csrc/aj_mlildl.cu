@@ -958,25 +958,52 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 // application kernels: G threads per row (G | 32), coalesced row segments,
 // shuffle reduction inside the group.  One row per group, no grid-stride
 // loop so every lane of a warp reaches the shuffles.
+// Programmatic dependent launch (PDL): every apply kernel lets its successor
+// launch immediately (griddepcontrol.launch_dependents) and loads everything that
+// does not depend on its predecessor -- row bounds, indices, factor values -- before
+// griddepcontrol.wait; only the gathers of the predecessor's output come after it.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+constexpr int PREF = 4;  // factor entries per lane prefetched before the dependency wait
+
 template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
     k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
                 const double* __restrict__ r, const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol,
                 const TV* __restrict__ Lval, double* __restrict__ rn) {
+  pdl_launch_dependents();
   const int gid = blockIdx.x * TB + threadIdx.x;
   const int cp = gid / G, lane = gid % G;
   const bool act = cp < nC;
+  int64_t e0 = 0, e1 = 0;
+  int c = 0;
+  double Dc = 0.0;
+  int32_t pc[PREF];
+  double pv[PREF];
+  if (act) {
+    e0 = Lptr[cp] + lane;
+    e1 = Lptr[cp + 1];
+    c = cidx[cp];
+    Dc = D[c];
+#pragma unroll
+    for (int q = 0; q < PREF; ++q) {
+      const int64_t e = e0 + (int64_t)q * G;
+      pc[q] = (e < e1) ? Lcol[e] : -1;
+      pv[q] = (e < e1) ? (double)Lval[e] : 0.0;
+    }
+  }
+  pdl_wait();
   double acc = 0.0;
   if (act) {
-    const int64_t e1 = Lptr[cp + 1];
-    for (int64_t e = Lptr[cp] + lane; e < e1; e += G) acc += (double)Lval[e] * __ldg(&r[Lcol[e]]);
+#pragma unroll
+    for (int q = 0; q < PREF; ++q)
+      if (pc[q] >= 0) acc += pv[q] * __ldg(&r[pc[q]]);
+    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)Lval[e] * __ldg(&r[Lcol[e]]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (act && lane == 0) {
-    const int c = cidx[cp];
-    rn[cp] = D[c] * r[c] - acc;
-  }
+  if (act && lane == 0) rn[cp] = Dc * r[c] - acc;
 }
 
 // backward substitution: blocks [0, bF) take the pivot (F) rows with G lanes
@@ -988,30 +1015,61 @@ __global__ void __launch_bounds__(TB)
                 const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ LTptr,
                 const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval, const double* __restrict__ zn,
                 double* __restrict__ z) {
+  pdl_launch_dependents();
   if ((int)blockIdx.x >= bF) {
     const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
+    int i = 0;
+    double Di = 0.0;
     if (cp < nC) {
-      const int i = cidx[cp];
-      z[i] = D[i] * zn[cp];
+      i = cidx[cp];
+      Di = D[i];
     }
+    pdl_wait();
+    if (cp < nC) z[i] = Di * zn[cp];
     return;
   }
   const int gid = blockIdx.x * TB + threadIdx.x;
   const int fp = gid / G, lane = gid % G;
   const bool act = fp < nF;
+  int64_t e0 = 0, e1 = 0;
+  int i = 0, p = -1;
+  double Di = 0.0, Dp = 0.0, B1 = 0.0, B2 = 0.0;
+  int32_t pc[PREF];
+  double pv[PREF];
+  if (act) {
+    e0 = LTptr[fp] + lane;
+    e1 = LTptr[fp + 1];
+#pragma unroll
+    for (int q = 0; q < PREF; ++q) {
+      const int64_t e = e0 + (int64_t)q * G;
+      pc[q] = (e < e1) ? LTcol[e] : -1;
+      pv[q] = (e < e1) ? (double)LTval[e] : 0.0;
+    }
+    if (lane == 0) {
+      i = fidx[fp];
+      Di = D[i];
+      B1 = b11[i];
+      p = partner[i];
+      if (p >= 0) {
+        Dp = D[p];
+        B2 = b12[i];
+      }
+    }
+  }
+  pdl_wait();
   double acc = 0.0;
   if (act) {
-    const int64_t e1 = LTptr[fp + 1];
-    for (int64_t e = LTptr[fp] + lane; e < e1; e += G) acc += (double)LTval[e] * __ldg(&zn[LTcol[e]]);
+#pragma unroll
+    for (int q = 0; q < PREF; ++q)
+      if (pc[q] >= 0) acc += pv[q] * __ldg(&zn[pc[q]]);
+    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)LTval[e] * __ldg(&zn[LTcol[e]]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (act && lane == 0) {
-    const int i = fidx[fp];
-    double y = b11[i] * (D[i] * r[i]);
-    const int32_t p = partner[i];
-    if (p >= 0) y += b12[i] * (D[p] * r[p]);
-    z[i] = D[i] * (y - acc);
+    double y = B1 * (Di * r[i]);
+    if (p >= 0) y += B2 * (Dp * r[p]);
+    z[i] = Di * (y - acc);
   }
 }
 
@@ -1021,46 +1079,73 @@ static int pick_group(double avg_len) {
   return g;
 }
 
-static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t st) {
-  if (v.nC == 0) return;
-  const int G = v.gf;
-  const int grid = std::max(1, ceil_div((int64_t)v.nC * G, TB));
-  switch (G) {
-#define F(GG)                                                                                                 \
-  case GG:                                                                                                    \
-    if (v.f32)                                                                                                \
-      k_apply_fwd<GG, float><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, (const float*)v.Lval, rn); \
-    else                                                                                                      \
-      k_apply_fwd<GG, double><<<grid, TB, 0, st>>>(v.nC, v.cidx, v.D, r, v.Lptr, v.Lcol, (const double*)v.Lval, rn); \
-    break;
-    F(1) F(2) F(4) F(8) F(16) F(32)
-#undef F
-  }
+template <typename K, typename... Args>
+static void launch_pdl(K kernel, int grid, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TB);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AJ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
   AJ_LAUNCHED();
 }
-static void launch_bwd(const Level& v, const double* r, const double* zn, double* z, cudaStream_t st) {
-  const int G = v.gb;
-  const int bF = ceil_div((int64_t)v.nF * G, TB);
-  const int grid = std::max(1, bF + ceil_div(v.nC, TB));
-  switch (G) {
-#define B(GG)                                                                                                  \
-  case GG:                                                                                                     \
-    if (v.f32)                                                                                                 \
-      k_apply_bwd<GG, float><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11, v.b12, \
-                                                  v.LTptr, v.LTcol, (const float*)v.LTval, zn, z);             \
-    else                                                                                                       \
-      k_apply_bwd<GG, double><<<grid, TB, 0, st>>>(v.nF, v.nC, bF, v.fidx, v.cidx, v.D, r, v.partner, v.b11,   \
-                                                   v.b12, v.LTptr, v.LTcol, (const double*)v.LTval, zn, z);    \
-    break;
-    B(1) B(2) B(4) B(8) B(16) B(32)
-#undef B
+
+template <int G>
+static void fwd_g(const Level& v, const double* r, double* rn, int grid, cudaStream_t st) {
+  if (v.f32)
+    launch_pdl(k_apply_fwd<G, float>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r,
+               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const float*)v.Lval, rn);
+  else
+    launch_pdl(k_apply_fwd<G, double>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r,
+               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const double*)v.Lval, rn);
+}
+template <int G>
+static void bwd_g(const Level& v, const double* r, const double* zn, double* z, int bF, int grid, cudaStream_t st) {
+  if (v.f32)
+    launch_pdl(k_apply_bwd<G, float>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
+               (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
+               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z);
+  else
+    launch_pdl(k_apply_bwd<G, double>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
+               (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
+               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z);
+}
+
+static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t st) {
+  if (v.nC == 0) return;
+  const int grid = std::max(1, ceil_div((int64_t)v.nC * v.gf, TB));
+  switch (v.gf) {
+    case 1: fwd_g<1>(v, r, rn, grid, st); break;
+    case 2: fwd_g<2>(v, r, rn, grid, st); break;
+    case 4: fwd_g<4>(v, r, rn, grid, st); break;
+    case 8: fwd_g<8>(v, r, rn, grid, st); break;
+    case 16: fwd_g<16>(v, r, rn, grid, st); break;
+    default: fwd_g<32>(v, r, rn, grid, st); break;
   }
-  AJ_LAUNCHED();
+}
+static void launch_bwd(const Level& v, const double* r, const double* zn, double* z, cudaStream_t st) {
+  const int bF = ceil_div((int64_t)v.nF * v.gb, TB);
+  const int grid = std::max(1, bF + ceil_div(v.nC, TB));
+  switch (v.gb) {
+    case 1: bwd_g<1>(v, r, zn, z, bF, grid, st); break;
+    case 2: bwd_g<2>(v, r, zn, z, bF, grid, st); break;
+    case 4: bwd_g<4>(v, r, zn, z, bF, grid, st); break;
+    case 8: bwd_g<8>(v, r, zn, z, bF, grid, st); break;
+    case 16: bwd_g<16>(v, r, zn, z, bF, grid, st); break;
+    default: bwd_g<32>(v, r, zn, z, bF, grid, st); break;
+  }
 }
 
 // z = G r (dense, warp per row)
 __global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __restrict__ r,
                            double* __restrict__ z) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * TB + threadIdx.x) >> 5; i < n; i += (gridDim.x * TB) >> 5) {
     double acc = 0.0;
@@ -1377,15 +1462,15 @@ static double wall_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 (50/L)^2, tau_strong =
-// 10 tau_drop (R12; the paper scales its drop tolerance with the size too,
+// Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 min(1, (50/L)^2),
+// tau_strong = max(10 tau_drop, 5e-3) (R12; the paper scales its drop tolerance with the size too,
 // eps = 1/sqrt(N)).
 aj_precond_params resolve_params(const aj_precond_params& in, int L) {
   aj_precond_params P = in;
   const double sc = (50.0 / L) * (50.0 / L);
   if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
-  if (P.tau_strong < 0.0) P.tau_strong = 10.0 * P.tau_drop;
-  if (P.max_levels > 255) P.max_levels = 255;
+  if (P.tau_strong < 0.0) P.tau_strong = std::max(10.0 * P.tau_drop, 5e-3);
+  if (P.max_levels > 1023) P.max_levels = 1023;
   return P;
 }
 
@@ -1417,7 +1502,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
     k_lattice_csr<<<std::min(grid_for(n64), num_sms() * 16), TB, 0, st>>>(L, eps, hop, sigma, A.ptr, A.col,
                                                                            A.val);
     AJ_LAUNCHED();
-    for (int lev = 0; lev < P.max_levels && lev < 255; ++lev) {
+    for (int lev = 0; lev < P.max_levels && lev < 1023; ++lev) {
       if (A.n <= P.n_coarse_max) break;
       Level lv;
       Csr S;

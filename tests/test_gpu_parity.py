@@ -82,7 +82,7 @@ def test_spmv_plane_wave_gpu(gpu_lib):
 def resolved(p, L):
     """DESIGN.md R12 auto rule for negative drop parameters."""
     td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
-    ts = p.tau_strong if p.tau_strong >= 0 else 10 * td
+    ts = p.tau_strong if p.tau_strong >= 0 else max(10 * td, 5e-3)
     return td, ts
 
 

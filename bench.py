@@ -228,7 +228,10 @@ def big_roofline(binding, L, peak):
     out["spmv"] = {"ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_site": 24}
     try:
         t0 = time.perf_counter()
-        K = binding.Precond(eps, L, -1.0, 0.0)
+        # kernel-throughput pass: factor with the fixed L=50 production drop parameters so the
+        # pass stays bounded (the size-scaled defaults of R12 take minutes to factor at L=250)
+        pp = binding.default_precond_params(tau_drop=2e-3, tau_strong=2e-2)
+        K = binding.Precond(eps, L, -1.0, 0.0, pp)
         torch.cuda.synchronize()
         out["precond_setup_s"] = time.perf_counter() - t0
         info = K.info()
@@ -248,7 +251,8 @@ def big_roofline(binding, L, peak):
         gbs = by / (ms * 1e-3) / 1e9
         out["precond_apply"] = {"ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_apply": by,
                                 "levels": info["levels"], "coarse_n": info["coarse_n"],
-                                "nnz_L_per_site": info["nnz_L"] / n}
+                                "nnz_L_per_site": info["nnz_L"] / n, "tau_drop": info["tau_drop"],
+                                "tau_strong": info["tau_strong"]}
         K.free()
     except Exception as ex:  # report, do not hide
         out["precond_apply"] = {"error": str(ex)[:300]}

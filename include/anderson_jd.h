@@ -76,7 +76,7 @@ typedef struct {
   double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa);
                             < 0: auto, 2e-3 * min(1, (50/L)^2)                    */
   double tau_strong;     /* strong-coupling threshold of the independent sets;
-                            < 0: auto, max(10 * tau_drop, 5e-3)                   */
+                            < 0: auto, 10 * tau_drop                              */
   int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
   int32_t max_levels;    /* level cap (<= 1023)                                  */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */

@@ -14,11 +14,6 @@ namespace aj {
 thread_local int64_t g_launches = 0;
 
 // ---- live profiling ------------------------------------------------------
-struct ProfRec {
-  cudaEvent_t a, b;
-  int cat;
-  double bytes;
-};
 static thread_local bool g_prof_on = false;
 static thread_local std::vector<ProfRec> g_prof_open;
 static thread_local std::vector<cudaEvent_t> g_event_pool;
@@ -35,19 +30,58 @@ static cudaEvent_t pool_event() {
   return e;
 }
 
+// While a stream is being captured into a CUDA graph, the scope records
+// *external* event nodes (they fire on every graph launch) and registers the pair
+// with the capturing code (g_prof_capture), which accumulates them per launch.
+static thread_local std::vector<ProfRec>* g_prof_capture = nullptr;
+
 ProfScope::ProfScope(int c, double by, cudaStream_t s) : cat(c), bytes(by), st(s), rec(nullptr) {
   if (!g_prof_on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  AJ_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs == cudaStreamCaptureStatusActive && !g_prof_capture) return;  // capture without a sink
   ProfRec* r = new ProfRec{pool_event(), pool_event(), c, by};
-  AJ_CUDA(cudaEventRecord(r->a, s));
+  if (cs == cudaStreamCaptureStatusActive)
+    AJ_CUDA(cudaEventRecordWithFlags(r->a, s, cudaEventRecordExternal));
+  else
+    AJ_CUDA(cudaEventRecord(r->a, s));
   rec = r;
 }
 ProfScope::~ProfScope() {
   if (!rec) return;
   ProfRec* r = (ProfRec*)rec;
-  cudaEventRecord(r->b, st);
-  g_prof_open.push_back(*r);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) {
+    cudaEventRecordWithFlags(r->b, st, cudaEventRecordExternal);
+    g_prof_capture->push_back(*r);
+  } else {
+    cudaEventRecord(r->b, st);
+    g_prof_open.push_back(*r);
+  }
   delete r;
 }
+
+void prof_set_capture_sink(std::vector<ProfRec>* sink) { g_prof_capture = sink; }
+// accumulate the event pairs of one completed graph launch
+void prof_accumulate(const std::vector<ProfRec>& recs) {
+  if (!g_prof_on) return;
+  for (const auto& r : recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+    g_prof_acc.ms[r.cat] += ms;
+    g_prof_acc.bytes[r.cat] += r.bytes;
+    g_prof_acc.calls[r.cat] += 1;
+  }
+}
+void prof_release(std::vector<ProfRec>& recs) {
+  for (auto& r : recs) {
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  recs.clear();
+}
+bool prof_enabled() { return g_prof_on; }
 
 static void prof_resolve() {
   for (auto& r : g_prof_open) {

@@ -82,7 +82,7 @@ void aj_precond_default_params(aj_precond_params* p) {
   if (!p) return;
   p->kappa = 5.0;
   p->tau_drop = -1.0;      // auto: 2e-3 (50/L)^2 (R12)
-  p->tau_strong = -1.0;    // auto: max(10 tau_drop, 5e-3)
+  p->tau_strong = -1.0;    // auto: 10 tau_drop
   p->n_coarse_max = 1024;
   p->max_levels = 1023;
   p->stall_frac = 0.005;

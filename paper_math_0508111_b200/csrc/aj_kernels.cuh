@@ -1,5 +1,7 @@
 // Internal launch interfaces of the Anderson JD library.
 #pragma once
+#include <vector>
+
 #include "aj_common.cuh"
 
 namespace aj {
@@ -47,5 +49,14 @@ void launch_fill(double* y, double v, int64_t n, cudaStream_t st);
 
 void prof_enable(bool on);
 void prof_get(aj_prof* out);
+struct ProfRec {
+  cudaEvent_t a, b;
+  int cat;
+  double bytes;
+};
+void prof_set_capture_sink(std::vector<ProfRec>* sink);
+void prof_accumulate(const std::vector<ProfRec>& recs);
+void prof_release(std::vector<ProfRec>& recs);
+bool prof_enabled();
 
 }  // namespace aj

@@ -1463,13 +1463,13 @@ static double wall_ms() {
 }
 
 // Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 min(1, (50/L)^2),
-// tau_strong = max(10 tau_drop, 5e-3) (R12; the paper scales its drop tolerance with the size too,
+// tau_strong = 10 tau_drop (R12; the paper scales its drop tolerance with the size too,
 // eps = 1/sqrt(N)).
 aj_precond_params resolve_params(const aj_precond_params& in, int L) {
   aj_precond_params P = in;
   const double sc = (50.0 / L) * (50.0 / L);
   if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
-  if (P.tau_strong < 0.0) P.tau_strong = std::max(10.0 * P.tau_drop, 5e-3);
+  if (P.tau_strong < 0.0) P.tau_strong = 10.0 * P.tau_drop;
   if (P.max_levels > 1023) P.max_levels = 1023;
   return P;
 }
@@ -1798,9 +1798,11 @@ void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st) 
   }
   const Level& v0 = K->lv[0];
   launch_fwd(v0, r, (nl > 1) ? K->lv[1].r : K->rc, st);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  AJ_CUDA(cudaStreamIsCapturing(st, &cs));
   if (K->tail_grid > 0) {
     launch_tail(K, st);
-  } else if (K->exec) {
+  } else if (K->exec && cs != cudaStreamCaptureStatusActive) {
     AJ_CUDA(cudaGraphLaunch(K->exec, st));
     g_launches += K->graph_nodes;
   } else {

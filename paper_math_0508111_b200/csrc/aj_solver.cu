@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -332,12 +333,22 @@ __global__ void k_negate_proj(int64_t n, double* __restrict__ b, const double* _
 // ============================================================================
 Workspace::Workspace(int64_t n_, cudaStream_t st) : n(n_) {
   rs.init(st);
+  AJ_CUDA(cudaMallocHost(&hpin, 64 * sizeof(double)));
+  AJ_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+  // opt-in (AJ_SQMR_GRAPH=1): capturing two graphs per correction equation costs more
+  // than it saves at ~20 SQMR steps per solve (L=50 step 361 vs 337 ms)
+  const char* e = getenv("AJ_SQMR_GRAPH");
+  use_graphs = (e && atoi(e) == 1);
   sc = dalloc<double>(S_COUNT, st);
   small = dalloc<double>(8192, st);
   for (int i = 0; i < 9; ++i) vec[i] = dalloc<double>(n, st);
 }
 void Workspace::release(cudaStream_t st) {
   rs.release(st);
+  if (hpin) cudaFreeHost(hpin);
+  hpin = nullptr;
+  if (cap_stream) cudaStreamDestroy(cap_stream);
+  cap_stream = nullptr;
   dfree(sc, st);
   dfree(small, st);
   for (int i = 0; i < 9; ++i) dfree(vec[i], st);
@@ -379,44 +390,103 @@ SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, doub
     return res;
   }
   const double sig_total = shift;  // operator A - (sigma + shift) I; caller folds sigma in
-  auto precond_proj = [&](int step) {
+  auto precond_proj = [&](int step, cudaStream_t s2) {
     // w = K^{-1} r ; q = (w - Y Hinv Q~^T w) + beta q ; rho
     if (K)
-      precond_run(K, w, r, st);
+      precond_run(K, w, r, s2);
     else
-      launch_copy(w, r, n, st);
-    if (m > 0) launch_multi_dot(dQw, Qt, m, n, w, n, ws.rs, st);
-    launch_multi_dot(dYr, Y, m + 1, n, r, n, ws.rs, st);
+      launch_copy(w, r, n, s2);
+    if (m > 0) launch_multi_dot(dQw, Qt, m, n, w, n, ws.rs, s2);
+    launch_multi_dot(dYr, Y, m + 1, n, r, n, ws.rs, s2);
     double* rho_out = sc + ((step & 1) ? S_RHO1 : S_RHO0);
     const double* rho_prev = sc + ((step & 1) ? S_RHO0 : S_RHO1);
-    ProfScope ps(PROF_SQMR, 8.0 * n * (m + 3), st);
-    k_sqmr_F<<<sgrid(n), TB, 0, st>>>(n, m, Y, w, q, dQw, dYr, Hinv, rho_prev, rho_out, step == 0 ? 1 : 0, sc);
+    ProfScope ps(PROF_SQMR, 8.0 * n * (m + 3), s2);
+    k_sqmr_F<<<sgrid(n), TB, 0, s2>>>(n, m, Y, w, q, dQw, dYr, Hinv, rho_prev, rho_out, step == 0 ? 1 : 0, sc);
     AJ_LAUNCHED();
   };
-  precond_proj(0);
+  precond_proj(0, st);
   int it = 0;
   double relres = 1.0;
-  for (it = 1; it <= maxit; ++it) {
-    // t = (A - sig I) q with fused [Q~ | q]^T t
-    launch_spmv_dots(t, q, eps, L, hop, sig_total, Qt, n, m + 1, ws.rs.buf(dA, 0), st);
-    const double* rho_cur = sc + (((it - 1) & 1) ? S_RHO1 : S_RHO0);
+  // One SQMR step (fused stencil + dots, the two update kernels, the residual
+  // readback and the next projected preconditioning) is captured into a CUDA
+  // graph per parity of the step (the rho slots alternate); the host launches one
+  // graph and reads the pinned residual per step.
+  auto body = [&](int p, cudaStream_t s2) {
+    launch_spmv_dots(t, q, eps, L, hop, sig_total, Qt, n, m + 1, ws.rs.buf(dA, 0), s2);
+    const double* rho_cur = sc + ((p ^ 1) ? S_RHO1 : S_RHO0);
     {
-      ProfScope ps(PROF_SQMR, 8.0 * n * (m + 4 + 10), st);
-      k_sqmr_B<<<sgrid(n), TB, 0, st>>>(n, m, Qt, t, r, dA, rho_cur, sc, ws.rs.buf(red, 1));
+      ProfScope ps(PROF_SQMR, 8.0 * n * (m + 4 + 10), s2);
+      k_sqmr_B<<<sgrid(n), TB, 0, s2>>>(n, m, Qt, t, r, dA, rho_cur, sc, ws.rs.buf(red, 1));
       AJ_LAUNCHED();
-      k_sqmr_C<<<sgrid(n), TB, 0, st>>>(n, q, t, d, x, sv, rx, sc, ws.rs.buf(red + 8, 2));
+      k_sqmr_C<<<sgrid(n), TB, 0, s2>>>(n, q, t, d, x, sv, rx, sc, ws.rs.buf(red + 8, 2));
       AJ_LAUNCHED();
     }
-    AJ_CUDA(cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    AJ_CUDA(cudaStreamSynchronize(st));
-    relres = sqrt(hs[S_RX2]) / nb;
-    if (hs[S_BRK] != 0.0) {
-      res.breakdown = true;
-      break;
+    AJ_CUDA(cudaMemcpyAsync(ws.hpin, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s2));
+  };
+  const bool use_graph = ws.use_graphs && maxit >= 4;
+  cudaGraphExec_t gx[2] = {nullptr, nullptr};
+  std::vector<ProfRec> gprof[2];
+  int64_t gnodes[2] = {0, 0};
+  auto cleanup_graphs = [&]() {
+    for (int p = 0; p < 2; ++p) {
+      if (gx[p]) cudaGraphExecDestroy(gx[p]);
+      gx[p] = nullptr;
+      prof_release(gprof[p]);
     }
-    if (relres <= tol || it == maxit) break;
-    precond_proj(it);
+  };
+  try {
+    if (use_graph) {
+      for (int p = 0; p < 2; ++p) {
+        const int64_t before = g_launches;
+        // capture on the workspace's private stream (the caller's stream may be the
+        // legacy default stream, which cannot be captured); launches go to `st`
+        const cudaStream_t cs = ws.cap_stream;
+        prof_set_capture_sink(&gprof[p]);
+        AJ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        body(p, cs);
+        precond_proj(p == 0 ? 2 : 1, cs);  // any step of that parity (step > 0)
+        cudaGraph_t g;
+        const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+        prof_set_capture_sink(nullptr);
+        AJ_CUDA(ec);
+        AJ_CUDA(cudaGraphInstantiate(&gx[p], g, 0));
+        AJ_CUDA(cudaGraphDestroy(g));
+        gnodes[p] = g_launches - before;
+        g_launches = before;
+      }
+    }
+    for (it = 1; it <= maxit; ++it) {
+      const int p = it & 1;
+      if (use_graph) {
+        AJ_CUDA(cudaGraphLaunch(gx[p], st));
+        g_launches += gnodes[p];
+        AJ_CUDA(cudaStreamSynchronize(st));
+        prof_accumulate(gprof[p]);
+      } else {
+        body(p, st);
+        AJ_CUDA(cudaStreamSynchronize(st));
+      }
+      const double* hs2 = ws.hpin;
+      relres = sqrt(hs2[S_RX2]) / nb;
+      if (hs2[S_BRK] != 0.0) {
+        res.breakdown = true;
+        break;
+      }
+      if (relres <= tol || it == maxit) break;
+      if (!use_graph) precond_proj(it, st);
+    }
+  } catch (...) {
+    prof_set_capture_sink(nullptr);
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(ws.cap_stream, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(ws.cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+    }
+    cleanup_graphs();
+    throw;
   }
+  cleanup_graphs();
   res.iters = std::min(it, maxit);
   res.relres = relres;
   return res;

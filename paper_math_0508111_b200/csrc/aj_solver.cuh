@@ -12,6 +12,9 @@ struct Workspace {
   double* sc = nullptr;     // SQMR scalars
   double* small = nullptr;  // dot outputs / small matrices
   double* vec[9] = {};      // n-vectors: r, t, d, s, rx + spare
+  double* hpin = nullptr;   // pinned host copy of the SQMR scalars
+  bool use_graphs = false;  // SQMR step as a CUDA graph (opt-in: AJ_SQMR_GRAPH=1)
+  cudaStream_t cap_stream = nullptr;  // private stream used only for graph capture
   Workspace(int64_t n_, cudaStream_t st);
   void release(cudaStream_t st);
 };

@@ -82,7 +82,7 @@ def test_spmv_plane_wave_gpu(gpu_lib):
 def resolved(p, L):
     """DESIGN.md R12 auto rule for negative drop parameters."""
     td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
-    ts = p.tau_strong if p.tau_strong >= 0 else max(10 * td, 5e-3)
+    ts = p.tau_strong if p.tau_strong >= 0 else 10 * td
     return td, ts
 
 
@@ -328,3 +328,20 @@ def test_jd_config2_l100_properties(gpu_lib):
     jp = gpu_lib.default_jd_params(seed=12345)
     lam2, X2, res2, st2 = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop, jparams=jp)
     assert np.allclose(np.sort(lam1), np.sort(lam2), atol=1e-10 * normA)
+
+
+def test_sqmr_graph_path_agrees(gpu_lib, monkeypatch):
+    # the optional captured SQMR step (AJ_SQMR_GRAPH=1) runs the same arithmetic
+    import torch
+    L, hop, sigma = 12, -1.0, 0.0
+    eps = gpu_eps(gpu_lib, L, 16.5, 3)
+    K = gpu_lib.Precond(eps, L, hop, sigma)
+    b = T(rand_vec(L ** 3, 6))
+    x1 = torch.empty_like(b)
+    _, it1, rel1, _ = gpu_lib.sqmr_solve(K, x1, b, eps, L, hop, sigma, tol=1e-10, maxit=200)
+    monkeypatch.setenv("AJ_SQMR_GRAPH", "1")
+    x2 = torch.empty_like(b)
+    _, it2, rel2, _ = gpu_lib.sqmr_solve(K, x2, b, eps, L, hop, sigma, tol=1e-10, maxit=200)
+    assert it1 == it2 and rel2 <= 1e-10
+    assert torch.linalg.norm(x1 - x2) <= 1e-13 * torch.linalg.norm(x1)
+    K.free()

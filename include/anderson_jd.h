@@ -185,8 +185,10 @@ AJ_API int64_t aj_launch_count(int32_t reset);
  * Categories: 0 stencil SpMV (incl. fused dots), 1 preconditioner apply,
  * 2 preconditioner setup, 3 SQMR vector updates, 4 JD subspace kernels.
  * bytes = algorithmic HBM bytes of the recorded calls (DESIGN.md sect. 4).
- * aj_prof_enable(1) resets and starts, (0) stops; aj_prof_get synchronises
- * the device and returns the totals of this thread.
+ * aj_prof_enable(1) resets and starts recording every category, (0) stops;
+ * aj_prof_enable(0x80000000 | mask) records only the categories of `mask`
+ * (bit c = category c).  aj_prof_get synchronises the device and returns the
+ * totals of this thread.
  * ------------------------------------------------------------------------- */
 #define AJ_PROF_CATS 8
 typedef struct {

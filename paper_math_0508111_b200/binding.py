@@ -265,8 +265,16 @@ def launch_count(reset=False):
     return lib().aj_launch_count(1 if reset else 0)
 
 
-def prof_enable(on=True):
-    _check(lib().aj_prof_enable(1 if on else 0))
+def prof_enable(on=True, categories=None):
+    """Start/stop live per-phase timing; `categories` restricts it to the named
+    phases (cheaper: the JD/SQMR vector kernels are thousands of tiny calls)."""
+    if on and categories:
+        mask = 0
+        for c in categories:
+            mask |= 1 << PROF_CATS.index(c)
+        _check(lib().aj_prof_enable(ctypes.c_int32(-0x80000000 | mask).value))
+    else:
+        _check(lib().aj_prof_enable(1 if on else 0))
 
 
 def prof_get():

@@ -35,11 +35,12 @@ static cudaEvent_t pool_event() {
 // with the capturing code (g_prof_capture), which accumulates them per launch.
 static thread_local std::vector<ProfRec>* g_prof_capture = nullptr;
 
+static thread_local unsigned g_prof_mask = ~0u;
+
 ProfScope::ProfScope(int c, double by, cudaStream_t s) : cat(c), bytes(by), st(s), rec(nullptr) {
-  if (!g_prof_on) return;
+  if (!g_prof_on || !((g_prof_mask >> c) & 1u)) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  AJ_CUDA(cudaStreamIsCapturing(s, &cs));
-  if (cs == cudaStreamCaptureStatusActive && !g_prof_capture) return;  // capture without a sink
+  if (g_prof_capture) AJ_CUDA(cudaStreamIsCapturing(s, &cs));  // only capturing code installs a sink
   ProfRec* r = new ProfRec{pool_event(), pool_event(), c, by};
   if (cs == cudaStreamCaptureStatusActive)
     AJ_CUDA(cudaEventRecordWithFlags(r->a, s, cudaEventRecordExternal));
@@ -51,7 +52,7 @@ ProfScope::~ProfScope() {
   if (!rec) return;
   ProfRec* r = (ProfRec*)rec;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(st, &cs);
+  if (g_prof_capture) cudaStreamIsCapturing(st, &cs);
   if (cs == cudaStreamCaptureStatusActive) {
     cudaEventRecordWithFlags(r->b, st, cudaEventRecordExternal);
     g_prof_capture->push_back(*r);
@@ -97,10 +98,11 @@ static void prof_resolve() {
   g_prof_open.clear();
 }
 
-void prof_enable(bool on) {
+void prof_enable(bool on, unsigned mask) {
   if (on) {
     prof_resolve();
     memset(&g_prof_acc, 0, sizeof(g_prof_acc));
+    g_prof_mask = mask ? mask : ~0u;
   }
   g_prof_on = on;
 }

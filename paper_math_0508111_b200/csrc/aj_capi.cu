@@ -48,7 +48,9 @@ int64_t aj_launch_count(int32_t reset) {
 
 int aj_prof_enable(int32_t on) {
   return guarded("aj_prof_enable", [&] {
-    aj::prof_enable(on != 0);
+    // on: 1 = all categories, or a category bit mask (bit c = category c) with bit 31 set
+    const unsigned mask = (on & 0x80000000) ? (unsigned)on & 0x7fffffffu : 0u;
+    aj::prof_enable(on != 0, mask);
     return AJ_OK;
   });
 }

@@ -47,7 +47,7 @@ void launch_normalize(double* x, const double* nrm2, int64_t n, cudaStream_t st)
 void launch_copy(double* y, const double* x, int64_t n, cudaStream_t st);
 void launch_fill(double* y, double v, int64_t n, cudaStream_t st);
 
-void prof_enable(bool on);
+void prof_enable(bool on, unsigned mask = 0);
 void prof_get(aj_prof* out);
 struct ProfRec {
   cudaEvent_t a, b;

@@ -76,13 +76,18 @@ typedef struct {
   double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa);
                             < 0: auto, 2e-3 * min(1, (50/L)^2)                    */
   double tau_strong;     /* strong-coupling threshold of the independent sets;
-                            < 0: auto, 10 * tau_drop                              */
+                            < 0: auto, min(0.05, 40 tau_drop) with compensation,
+                            else 10 * tau_drop                                    */
   int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
   int32_t max_levels;    /* level cap (<= 1023)                                  */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
   int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN)      */
   int32_t cand_cap;      /* reserved (>= 64)                                     */
   int32_t factor_fp32;   /* 1: store L / L^T values in fp32 (fp64 accumulation)  */
+  int32_t compensate;    /* 1: first-order treatment of the dropped weak pivot-pivot
+                            couplings, B^{-1} ~ B_d^{-1} - B_d^{-1} E B_d^{-1} (R17) */
+  double tau_virtual;    /* only couplings |a^_uv| >= tau_virtual are compensated;
+                            < 0: auto, 5 * tau_drop (R17)                           */
 } aj_precond_params;
 
 typedef struct {
@@ -97,6 +102,8 @@ typedef struct {
   double setup_ms;        /* device time of precond_setup                         */
   double tau_drop;        /* resolved drop tolerance                              */
   double tau_strong;      /* resolved strong-coupling threshold                   */
+  double tau_virtual;     /* resolved compensation threshold (0 if compensate=0)  */
+  int64_t nnz_V;          /* virtual 2x2 blocks over all levels (R17)             */
 } aj_precond_info;
 
 AJ_API void aj_precond_default_params(aj_precond_params* p);

@@ -163,7 +163,8 @@ def _mis(nb, keyrank, edges_a, edges_b):
     return sel, rounds
 
 
-def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.005):
+def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.005, compensate=True,
+                 tau_virtual=None):
     n = A.shape[0]
     D, Ah = _scaled(A)
     dg, lmax1, d1, p = _pivot_quality(Ah)
@@ -266,76 +267,176 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
     Lv.npairs = int(((partner >= 0) & inF).sum() // 2)
     Lv.rounds = rounds
     Lv.repair_rounds = repair_rounds
-    Lfull = _lfull(Ah, inF, partner, b11, b12, dg)          # rows: level idx (C only)
-    Lc = Lfull.tocoo()
-    keep = np.abs(Lc.data) >= tau_drop
     cmap = np.full(n, -1, dtype=np.int64)
     cmap[Lv.C] = np.arange(len(Lv.C))
     Lv.cmap = cmap
-    # L stored with rows = coarse index, cols = level index (F nodes)
-    Lv.L = sp.csr_matrix((Lc.data[keep], (cmap[Lc.row[keep]], Lc.col[keep])), shape=(len(Lv.C), n))
-    Lv.L.sort_indices()
-    Lv.S = _schur(Ah, inF, partner, b11, b12, Lv.C, cmap, tau_drop)
-    Lv.Binv = _binv(n, inF, partner, b11, b12)
+    tv = 5.0 * tau_drop if tau_virtual is None else tau_virtual
+    blocks = _blocks(Ah, inF, partner, b11, b12, compensate, tv)
+    Lv.nvirtual = int((blocks["kind"] == 2).sum())
+    inc = _incidence(Ah, inF, blocks)
+    Lv.L = _l_rows(inc, blocks, n, cmap, len(Lv.C), tau_drop)
+    Lv.S = _schur_blocks(Ah, inF, inc, blocks, Lv.C, cmap, tau_drop)
+    Lv.Binv = _binv_blocks(n, blocks)
     return Lv
 
 
-def _schur(Ah, inF, partner, b11, b12, C, cmap, tau_drop):
-    """S = A^_CC - A^_CF B^{-1} A^_FC, reading R10:
-    s_cc' = a^_cc' - sum_{blocks b adjacent to c and c', ascending leader} T_b(c, c') with
-      1x1 {f}:    T = B_ff (a_cf a_c'f)
-      2x2 {f,g}:  T = (B_ff (a_cf a_c'f) + B_gg (a_cg a_c'g)) + B_fg ((a_cf a_c'g) + (a_cg a_c'f))
-    (symmetric in c, c' term by term), then off-diagonals |s| < tau_drop dropped."""
+def _blocks(Ah, inF, partner, b11, b12, compensate, tau_virtual=0.0):
+    """Pivot blocks of a level plus, with `compensate` (reading R17), one virtual
+    2x2 block per coupling |a^_uv| >= tau_virtual between two pivot singles u < v: B' = [[0, b'],
+    [b', 0]], b' = -(a^_uv (B_uu B_vv)) -- the first-order term of
+    B^{-1} = (B_d + E)^{-1} ~ B_d^{-1} - B_d^{-1} E B_d^{-1}.  Key = (lmin, lmax)."""
+    n = Ah.shape[0]
+    F = np.where(inF)[0]
+    rows = []
+    for f in F:
+        g = partner[f]
+        if g < 0:
+            rows.append((f, f, f, -1, b11[f], 0.0, 0.0, 0))
+        elif f < g:
+            rows.append((f, g, f, g, b11[f], b12[f], b11[g], 1))
+    if compensate:
+        coo = Ah.tocoo()
+        r, c, v = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
+        m = (r < c) & inF[r] & inF[c] & (partner[r] < 0) & (partner[c] < 0) & (np.abs(v) >= tau_virtual)
+        for u, w, a in zip(r[m], c[m], v[m]):
+            rows.append((u, w, u, w, 0.0, -(a * (b11[u] * b11[w])), 0.0, 2))
+    a = np.array(rows, dtype=object) if rows else np.zeros((0, 8), dtype=object)
+    blk = {}
+    blk["kmin"] = np.array([x[0] for x in rows], dtype=np.int64)
+    blk["kmax"] = np.array([x[1] for x in rows], dtype=np.int64)
+    blk["f"] = np.array([x[2] for x in rows], dtype=np.int64)
+    blk["g"] = np.array([x[3] for x in rows], dtype=np.int64)
+    blk["Bff"] = np.array([x[4] for x in rows], dtype=np.float64)
+    blk["Bfg"] = np.array([x[5] for x in rows], dtype=np.float64)
+    blk["Bgg"] = np.array([x[6] for x in rows], dtype=np.float64)
+    blk["kind"] = np.array([x[7] for x in rows], dtype=np.int64)
+    blk["key"] = blk["kmin"] * n + blk["kmax"]
+    del a
+    return blk
+
+
+def _incidence(Ah, inF, blk):
+    """Elements (C row c, block b) for every block with a member adjacent to c:
+    a_cf, a_cg = a^ from c to the block's first / second member (0 if absent)."""
+    n = Ah.shape[0]
+    coo = Ah.tocoo()
+    r, c, v = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
+    m = (~inF[r]) & inF[c]
+    rc, uc, av = r[m], c[m], v[m]
+    nb = len(blk["f"])
+    # member -> blocks containing it (as first or second member)
+    mem_b = np.concatenate([np.arange(nb), np.arange(nb)[blk["g"] >= 0]])
+    mem_x = np.concatenate([blk["f"], blk["g"][blk["g"] >= 0]])
+    mem_pos = np.concatenate([np.zeros(nb, np.int64), np.ones(int((blk["g"] >= 0).sum()), np.int64)])
+    o = np.argsort(mem_x, kind="stable")
+    mem_b, mem_x, mem_pos = mem_b[o], mem_x[o], mem_pos[o]
+    start = np.searchsorted(mem_x, uc, side="left")
+    stop = np.searchsorted(mem_x, uc, side="right")
+    cnt = stop - start
+    rep = np.repeat(np.arange(len(uc)), cnt)
+    off = np.arange(len(rep)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    idx = np.repeat(start, cnt) + off
+    e_c, e_b, e_pos, e_a = rc[rep], mem_b[idx], mem_pos[idx], av[rep]
+    key = e_c * nb + e_b
+    uk, inv = _unique_inverse(key)
+    acf = np.zeros(len(uk))
+    acg = np.zeros(len(uk))
+    acf[inv[e_pos == 0]] = e_a[e_pos == 0]
+    acg[inv[e_pos == 1]] = e_a[e_pos == 1]
+    return dict(c=uk // nb, b=uk % nb, acf=acf, acg=acg)
+
+
+def _l_rows(inc, blk, n, cmap, nC, tau_drop):
+    """L = A^_CF B~^{-1}: l_cx = sum over blocks b containing x (ascending key) of
+    [(a_cf, a_cg) B_b]_x, accumulated from 0; |l| < tau_drop dropped."""
+    b = inc["b"]
+    f, g = blk["f"][b], blk["g"][b]
+    Bff, Bfg, Bgg = blk["Bff"][b], blk["Bfg"][b], blk["Bgg"][b]
+    acf, acg = inc["acf"], inc["acg"]
+    single = g < 0
+    vf = np.where(single, acf * Bff, acf * Bff + acg * Bfg)
+    vg = acf * Bfg + acg * Bgg
+    rows = np.concatenate([inc["c"], inc["c"][~single]])
+    cols = np.concatenate([f, g[~single]])
+    vals = np.concatenate([vf, vg[~single]])
+    keys = np.concatenate([blk["key"][b], blk["key"][b][~single]])
+    o = np.lexsort((keys, cols, rows))
+    rows, cols, vals = rows[o], cols[o], vals[o]
+    rk = rows * n + cols
+    uk, inv = _unique_inverse(rk)
+    acc = np.zeros(len(uk))
+    np.add.at(acc, inv, vals)              # sequential in ascending block key
+    lr, lc = uk // n, uk % n
+    keep = np.abs(acc) >= tau_drop
+    L = sp.csr_matrix((acc[keep], (cmap[lr[keep]], lc[keep])), shape=(nC, n))
+    L.sort_indices()
+    return L
+
+
+def _schur_blocks(Ah, inF, inc, blk, C, cmap, tau_drop):
+    """S = A^_CC - A^_CF B~^{-1} A^_FC, readings R10/R17:
+    s_cc' = a^_cc' - sum_{blocks b adjacent to c and c', ascending key} T_b(c, c') with
+      1x1 {f}:      T = B_ff (a_cf a_c'f)
+      2-member:     T = (B_ff (a_cf a_c'f) + B_gg (a_cg a_c'g)) + B_fg ((a_cf a_c'g) + (a_cg a_c'f))
+    (symmetric in c, c' term by term), then off-diagonals |s| < tau_drop dropped.
+    Reading R17: the pattern of S is that of A^_CC and the real blocks' terms; the
+    virtual blocks' terms are subtracted after the real ones (ascending key) and only
+    on that pattern (the compensation creates no fill)."""
     n = Ah.shape[0]
     nC = len(C)
     coo = Ah.tocoo()
     r, c, v = coo.row, coo.col, coo.data
-    # entries (c in C, u in F): block leader f = min(u, partner), value to f / to g
-    m = (~inF[r]) & inF[c]
-    rc, uc, av = r[m].astype(np.int64), c[m].astype(np.int64), v[m]
-    lead = np.where(partner[uc] >= 0, np.minimum(uc, partner[uc]), uc)
-    key = rc * n + lead
-    uk, inv = _unique_inverse(key)
-    acf = np.zeros(len(uk))
-    acg = np.zeros(len(uk))
-    isf = uc == lead
-    acf[inv[isf]] = av[isf]
-    acg[inv[~isf]] = av[~isf]
-    ec, el = uk // n, uk % n                         # element = (C row, block leader)
-    o = np.lexsort((ec, el))                         # group by leader
-    ec, el, acf, acg = ec[o], el[o], acf[o], acg[o]
-    gstart = np.flatnonzero(np.r_[True, el[1:] != el[:-1]])
-    gcnt = np.diff(np.r_[gstart, len(el)])
+    ec, eb, acf, acg = inc["c"], inc["b"], inc["acf"], inc["acg"]
+    o = np.lexsort((ec, eb))                         # group elements by block
+    ec, eb, acf, acg = ec[o], eb[o], acf[o], acg[o]
+    if len(eb):
+        gstart = np.flatnonzero(np.r_[True, eb[1:] != eb[:-1]])
+        gcnt = np.diff(np.r_[gstart, len(eb)])
+    else:
+        gstart = np.zeros(0, np.int64)
+        gcnt = np.zeros(0, np.int64)
     gid = np.repeat(np.arange(len(gstart)), gcnt)
-    E = len(el)
     reps = gcnt[gid]
-    a_idx = np.repeat(np.arange(E), reps)
+    a_idx = np.repeat(np.arange(len(eb)), reps)
     before = np.repeat(np.cumsum(reps) - reps, reps)
     b_idx = gstart[gid[a_idx]] + (np.arange(len(a_idx)) - before)
-    f = el[a_idx]
-    g = partner[f]
-    Bff = b11[f]
+    bb = eb[a_idx]
+    single = blk["g"][bb] < 0
+    Bff, Bfg, Bgg = blk["Bff"][bb], blk["Bfg"][bb], blk["Bgg"][bb]
     A1, A2 = acf[a_idx], acf[b_idx]
     G1, G2 = acg[a_idx], acg[b_idx]
     T = Bff * (A1 * A2)
-    pm = g >= 0
-    gg = g[pm]
-    T[pm] = (Bff[pm] * (A1[pm] * A2[pm]) + b11[gg] * (G1[pm] * G2[pm])) + \
-        b12[f[pm]] * ((A1[pm] * G2[pm]) + (G1[pm] * A2[pm]))
+    pm = ~single
+    T[pm] = (Bff[pm] * (A1[pm] * A2[pm]) + Bgg[pm] * (G1[pm] * G2[pm])) + \
+        Bfg[pm] * ((A1[pm] * G2[pm]) + (G1[pm] * A2[pm]))
     tk = cmap[ec[a_idx]] * nC + cmap[ec[b_idx]]
-    # starting values a^_cc' on C x C (diagonal always present)
     mc = (~inF[r]) & (~inF[c])
     k0 = cmap[r[mc]] * nC + cmap[c[mc]]
-    keys = _unique(np.concatenate([k0, tk, np.arange(nC) * (nC + 1)]))
+    virt = blk["kind"][bb] == 2
+    keys = _unique(np.concatenate([k0, tk[~virt], np.arange(nC) * (nC + 1)]))
+    pos = np.minimum(np.searchsorted(keys, tk), max(len(keys) - 1, 0))
+    on = ~virt | (keys[pos] == tk)                   # virtual terms: pattern entries only
+    tk, T, bb, virt = tk[on], T[on], bb[on], virt[on]
     sval = np.zeros(len(keys))
     sval[np.searchsorted(keys, k0)] = v[mc]
-    ot = np.lexsort((f, tk))                         # per entry: ascending leader
+    ot = np.lexsort((blk["key"][bb], virt, tk))      # per entry: real, then virtual; ascending key
     np.subtract.at(sval, np.searchsorted(keys, tk[ot]), T[ot])
     sr, sc = keys // nC, keys % nC
     keep = (sr == sc) | (np.abs(sval) >= tau_drop)
     S = sp.csr_matrix((sval[keep], (sr[keep], sc[keep])), shape=(nC, nC))
     S.sort_indices()
     return S
+
+
+def _binv_blocks(n, blk):
+    """B~^{-1} on the pivot nodes: block inverses plus the virtual couplings."""
+    f, g = blk["f"], blk["g"]
+    two = g >= 0
+    rows = np.concatenate([f, g[two], f[two], g[two]])
+    cols = np.concatenate([f, g[two], g[two], f[two]])
+    vals = np.concatenate([blk["Bff"], blk["Bgg"][two], blk["Bfg"][two], blk["Bfg"][two]])
+    keep = vals != 0.0
+    return sp.csr_matrix((vals[keep], (rows[keep], cols[keep])), shape=(n, n))
 
 
 def _binv(n, inF, partner, b11, b12):
@@ -367,7 +468,8 @@ class MultilevelILDL:
     """M^{-1} ~ (A - sigma I)^{-1}; see module docstring."""
 
     def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
-                 n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False):
+                 n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False,
+                 compensate=True, tau_virtual=None):
         """factor_fp32 (reading R16): the stored factor values are rounded to
         IEEE binary32 -- forward entries as fl32(l_cf * D_f), backward entries as
         fl32(l_cf) -- and used in fp64 arithmetic, as on the GPU."""
@@ -379,7 +481,7 @@ class MultilevelILDL:
             if cur.shape[0] <= n_coarse_max:
                 break
             Lv = factor_level(cur, kappa, tau_drop, tau_strong,
-                              lattice_L if lev == 0 else None, stall_frac)
+                              lattice_L if lev == 0 else None, stall_frac, compensate, tau_virtual)
             if Lv is None:
                 break
             if self.factor_fp32:

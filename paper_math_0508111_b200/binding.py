@@ -31,19 +31,22 @@ class AJError(RuntimeError):
 class PrecondParams(ctypes.Structure):
     _fields_ = [("kappa", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
                 ("n_coarse_max", ctypes.c_int32), ("max_levels", ctypes.c_int32), ("stall_frac", ctypes.c_double),
-                ("dense_cap", ctypes.c_int32), ("cand_cap", ctypes.c_int32), ("factor_fp32", ctypes.c_int32)]
+                ("dense_cap", ctypes.c_int32), ("cand_cap", ctypes.c_int32), ("factor_fp32", ctypes.c_int32),
+                ("compensate", ctypes.c_int32), ("tau_virtual", ctypes.c_double)]
 
 
 class PrecondInfo(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("coarse_n", ctypes.c_int32), ("nnz_L", ctypes.c_int64),
                 ("nnz_A", ctypes.c_int64), ("level_n", ctypes.c_int32 * 1024), ("level_nF", ctypes.c_int32 * 1024),
                 ("level_pairs", ctypes.c_int32 * 1024), ("level_nnzS", ctypes.c_int64 * 1024),
-                ("setup_ms", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double)]
+                ("setup_ms", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
+                ("tau_virtual", ctypes.c_double), ("nnz_V", ctypes.c_int64)]
 
     def as_dict(self):
         nl = self.levels
         return dict(levels=nl, coarse_n=self.coarse_n, nnz_L=self.nnz_L, nnz_A=self.nnz_A,
-                    tau_drop=self.tau_drop, tau_strong=self.tau_strong,
+                    tau_drop=self.tau_drop, tau_strong=self.tau_strong, tau_virtual=self.tau_virtual,
+                    nnz_V=self.nnz_V,
                     level_n=list(self.level_n[:nl]), level_nF=list(self.level_nF[:nl]),
                     level_pairs=list(self.level_pairs[:nl]), level_nnzS=list(self.level_nnzS[:nl]),
                     setup_ms=self.setup_ms)

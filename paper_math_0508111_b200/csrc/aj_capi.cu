@@ -84,13 +84,15 @@ void aj_precond_default_params(aj_precond_params* p) {
   if (!p) return;
   p->kappa = 5.0;
   p->tau_drop = -1.0;      // auto: 2e-3 (50/L)^2 (R12)
-  p->tau_strong = -1.0;    // auto: 10 tau_drop
+  p->tau_strong = -1.0;    // auto: min(0.05, 40 tau_drop) (R17), 10 tau_drop without compensation
   p->n_coarse_max = 1024;
   p->max_levels = 1023;
   p->stall_frac = 0.005;
   p->dense_cap = 4096;
   p->cand_cap = 2048;
   p->factor_fp32 = 0;      // DESIGN.md R16: fp32 storage is opt-in (hurts at large L)
+  p->compensate = 1;       // DESIGN.md R17
+  p->tau_virtual = -1.0;   // auto: 5 tau_drop (R17)
 }
 
 int precond_setup(void** handle, const double* d_eps, int32_t L, double hop, double sigma,

@@ -464,16 +464,19 @@ __global__ void k_cflags(int n, const int8_t* __restrict__ inF, int32_t* __restr
 }
 __global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __restrict__ scan,
                        int32_t* __restrict__ cmap, int32_t* __restrict__ cidx, int32_t* __restrict__ fidx,
+                       int32_t* __restrict__ fmap,
                        int32_t* __restrict__ partner_out, const int32_t* __restrict__ partner,
                        double* __restrict__ b11, double* __restrict__ b12) {
   for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) {
     if (inF[i]) {
       cmap[i] = -1;
       fidx[i - scan[i]] = i;  // scan counts the C nodes before i
+      fmap[i] = i - scan[i];
       partner_out[i] = partner[i];
     } else {
       cmap[i] = scan[i];
       cidx[scan[i]] = i;
+      fmap[i] = -1;
       partner_out[i] = -1;
       b11[i] = 0.0;
       b12[i] = 0.0;
@@ -481,126 +484,52 @@ __global__ void k_cmap(int n, const int8_t* __restrict__ inF, const int32_t* __r
   }
 }
 
-// L rows (coarse c'): entries (u, l_cu * D_u) with |l_cu| >= tau_drop; SG lanes per row,
-// each lane writes its own entries after a group prefix sum of the lane counts
-template <bool FILL, typename TV>
-__global__ void k_L_rows(int nC, const int32_t* __restrict__ cidx, const int64_t* __restrict__ ptr,
-                         const int32_t* __restrict__ col, const double* __restrict__ ah,
-                         const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
-                         const double* __restrict__ b11, const double* __restrict__ b12,
-                         const double* __restrict__ D, double tau, int64_t* __restrict__ cnt_or_ptr,
-                         int32_t* __restrict__ Lcol, TV* __restrict__ Lval) {
-  const int gl = threadIdx.x & (SG - 1);
-  const unsigned msk = sg_mask();
-  for (int cp = (blockIdx.x * TB + threadIdx.x) / SG; cp < nC; cp += gridDim.x * (TB / SG)) {
-    const int c = cidx[cp];
-    int cnt = 0;
-    for_blocks_of_row(
-        c, ptr, col, ah, inF, partner, b11, b12,
-        [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
-          cnt += (fabs(lf) >= tau) + (g >= 0 && fabs(lg) >= tau);
-        },
-        gl, SG);
-    // inclusive scan of the lane counts inside the group
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < SG; o <<= 1) {
-      const int t = __shfl_up_sync(msk, incl, o, SG);
-      if (gl >= o) incl += t;
-    }
-    if (!FILL) {
-      const int tot = __shfl_sync(msk, incl, SG - 1, SG);
-      if (gl == 0) cnt_or_ptr[cp] = tot;
-      continue;
-    }
-    int64_t w = cnt_or_ptr[cp] + (incl - cnt);
-    for_blocks_of_row(
-        c, ptr, col, ah, inF, partner, b11, b12,
-        [&](int32_t f, int32_t g, double lf, double lg, int32_t) {
-          if (fabs(lf) >= tau) {
-            Lcol[w] = f;
-            Lval[w] = (TV)(lf * D[f]);
-            ++w;
-          }
-          if (g >= 0 && fabs(lg) >= tau) {
-            Lcol[w] = g;
-            Lval[w] = (TV)(lg * D[g]);
-            ++w;
-          }
-        },
-        gl, SG);
-  }
-}
-
-// L^T rows (F index f' -> node u = fidx[f']): entries (cmap[c], l_cu) over C nodes c
-// adjacent to u or its partner
-template <bool FILL, typename TV>
-__global__ void k_LT_rows(int nF, const int32_t* __restrict__ fidx, const int64_t* __restrict__ ptr,
-                          const int32_t* __restrict__ col, const double* __restrict__ ah,
-                          const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
-                          const double* __restrict__ b11, const double* __restrict__ b12,
-                          const int32_t* __restrict__ cmap, double tau, int64_t* __restrict__ cnt_or_ptr,
-                          int32_t* __restrict__ LTcol, TV* __restrict__ LTval) {
-  for (int fp = blockIdx.x * TB + threadIdx.x; fp < nF; fp += gridDim.x * TB) {
-    const int u = fidx[fp];
-    int64_t w = FILL ? cnt_or_ptr[fp] : 0;
-    const int32_t p = partner[u];
-    if (p < 0) {
-      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
-        const int32_t c = col[e];
-        if (c == u || inF[c]) continue;
-        const double l = __dmul_rn(ah[e], b11[u]);
-        if (fabs(l) >= tau) {
-          if (FILL) {
-            LTcol[w] = cmap[c];
-            LTval[w] = (TV)l;
-          }
-          ++w;
-        }
-      }
-    } else {
-      const int32_t f = min(u, p), g = max(u, p);
-      int64_t ef = ptr[f], eg = ptr[g];
-      const int64_t ef1 = ptr[f + 1], eg1 = ptr[g + 1];
-      while (ef < ef1 || eg < eg1) {
-        const int32_t cf = (ef < ef1) ? col[ef] : INT32_MAX;
-        const int32_t cg = (eg < eg1) ? col[eg] : INT32_MAX;
-        const int32_t c = min(cf, cg);
-        double a_cf = 0.0, a_cg = 0.0;
-        if (cf == c) a_cf = ah[ef++];
-        if (cg == c) a_cg = ah[eg++];
-        if (c == f || c == g || inF[c]) continue;
-        const double l = (u == f) ? lval_pair(a_cf, a_cg, b11[f], b12[g]) : lval_pair(a_cf, a_cg, b12[f], b11[g]);
-        if (fabs(l) >= tau) {
-          if (FILL) {
-            LTcol[w] = cmap[c];
-            LTval[w] = (TV)l;
-          }
-          ++w;
-        }
-      }
-    }
-    if (!FILL) cnt_or_ptr[fp] = w;
-  }
-}
-
 // ----------------------------------------------------------------------------
 // Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, symmetric by construction,
 // off-diagonals with |s| < tau dropped.  One warp per coarse row.
+// Virtual 2x2 blocks (reading R17): every stored coupling |a^_uv| >= tau_v between two pivot
+// singles u != v (weak by construction of the independent set) gets
+// b'_uv = -(a^_uv (B_uu B_vv)) (product ordered by index) -- the first-order term
+// of (B_d + E)^{-1}.  Lists per level node (only pivot singles have entries).
+template <bool FILL>
+__global__ void k_virtual(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                          const double* __restrict__ ah, const int8_t* __restrict__ inF,
+                          const int32_t* __restrict__ partner, const double* __restrict__ b11, double tau_v,
+                          int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ Vcol, double* __restrict__ Vval) {
+  for (int u = blockIdx.x * TB + threadIdx.x; u < n; u += gridDim.x * TB) {
+    int64_t w = FILL ? cnt_or_ptr[u] : 0;
+    if (inF[u] && partner[u] < 0) {
+      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+        const int32_t v = col[e];
+        if (v == u || !inF[v] || partner[v] >= 0 || fabs(ah[e]) < tau_v) continue;
+        if (FILL) {
+          const int32_t lo = min(u, v), hi = max(u, v);
+          Vcol[w] = v;
+          Vval[w] = -__dmul_rn(ah[e], __dmul_rn(b11[lo], b11[hi]));
+        }
+        ++w;
+      }
+    }
+    if (!FILL) cnt_or_ptr[u] = w;
+  }
+}
+
 constexpr int SW = 4;            // warps per CTA
-constexpr int BMAX = 96;         // F blocks adjacent to one row (shared-memory variant)
+constexpr int BMAX = 1024;       // F blocks (real + virtual) adjacent to one row (shared-memory variant)
 constexpr int HT = 2048;         // per-warp hash table, shared-memory variant (power of 2)
 constexpr int HTG = 32768;       // per-warp hash table, global-memory fallback variant
 constexpr int BMAXG = 2048;      // block list of the fallback variant
 struct BlkEnt {
   int32_t f, g, lead;
+  int64_t key;  // (kmin << 32) | kmax: real block (leader, leader), virtual block (u, v)
   double acf, acg, Bff, Bgg, Bfg;
 };
-constexpr size_t kSchurSmem = (size_t)SW * (HT * sizeof(int32_t) + HT * sizeof(double) + BMAX * sizeof(BlkEnt));
-// global scratch per warp: list/keys (T int32) + values (T doubles) [+ table for the fallback]
+constexpr size_t kSchurSmem = (size_t)SW * HT * (sizeof(int32_t) + sizeof(double));  // 2 CTAs per SM
+// global scratch per warp: list/keys (T int32) + values (T doubles) [+ table for the
+// fallback] + the block list and its key order
 template <int T, bool GLOBAL>
 constexpr size_t schur_scratch_words() {
-  return GLOBAL ? (size_t)T * (1 + 2 + 1 + 2) + (size_t)BMAXG * (sizeof(BlkEnt) / 4) : (size_t)T * 3;
+  return (size_t)T * (GLOBAL ? 6 : 3) + (size_t)(GLOBAL ? BMAXG : BMAX) * (sizeof(BlkEnt) / 4 + 1);
 }
 
 // bitonic sort of (key, value) pairs by key, one warp
@@ -648,6 +577,20 @@ __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int
   return -1;
 }
 
+// slot of `key` in a warp's table, or -1 if absent (no insertion)
+template <int T>
+__device__ __forceinline__ int hfind(const int32_t* tab, int32_t key) {
+  constexpr int BITS = (T == 2048) ? 11 : 15;
+  uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
+  for (int probe = 0; probe < T; ++probe) {
+    const int32_t k = tab[h];
+    if (k == key) return (int)h;
+    if (k == -1) return -1;
+    h = (h + 1) & (T - 1);
+  }
+  return -1;
+}
+
 // Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, scatter form (reading R10):
 // s_cc' starts at a^_cc', then the F blocks adjacent to c are applied one after
 // the other in ascending leader order; block b walks the rows of its members and
@@ -659,14 +602,17 @@ __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int
 // flagged in row_ovf and queued in ovf_list.  GLOBAL = true: the fallback over
 // ovf_list with T = 32768 tables in global memory.
 template <bool GLOBAL>
-__global__ void __launch_bounds__(SW * 32)
+__global__ void __launch_bounds__(SW * 32, 2)
     k_schur(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
             const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
             const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
-            const double* __restrict__ b11, const double* __restrict__ b12, double tau,
+            const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ Vptr,
+            const int32_t* __restrict__ Vcol, const double* __restrict__ Vval, double tau,
             int32_t* __restrict__ scratch_all, int64_t* __restrict__ row_cnt, int64_t* __restrict__ row_off,
             int32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, int64_t cap,
-            unsigned long long* __restrict__ cursor, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
+            unsigned long long* __restrict__ cursor, int64_t* __restrict__ lrow_cnt, int64_t* __restrict__ lrow_off,
+            int32_t* __restrict__ ltmp_col, double* __restrict__ ltmp_val, int64_t lcap,
+            unsigned long long* __restrict__ lcursor, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
             int* __restrict__ error) {
   constexpr int T = GLOBAL ? HTG : HT;
   constexpr int BM = GLOBAL ? BMAXG : BMAX;
@@ -679,15 +625,17 @@ __global__ void __launch_bounds__(SW * 32)
   double* vals;
   int32_t* tab;
   BlkEnt* blk;
+  int32_t* bperm;  // blocks in ascending key order (indices into blk)
   if constexpr (GLOBAL) {
     tab = wscr + 3 * T;                                         // T int32
     vals = reinterpret_cast<double*>(wscr + 4 * T);             // T doubles
     blk = reinterpret_cast<BlkEnt*>(wscr + 6 * T);
+    bperm = wscr + 6 * T + (size_t)BM * (sizeof(BlkEnt) / 4);
   } else {
     vals = reinterpret_cast<double*>(smem_raw) + (size_t)wid * T;
     tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)SW * T * sizeof(double)) + (size_t)wid * T;
-    blk = reinterpret_cast<BlkEnt*>(smem_raw + (size_t)SW * T * (sizeof(double) + sizeof(int32_t))) +
-          (size_t)wid * BM;
+    blk = reinterpret_cast<BlkEnt*>(wscr + 3 * T);
+    bperm = wscr + 3 * T + (size_t)BM * (sizeof(BlkEnt) / 4);
   }
   for (int t = lane; t < T; t += 32) tab[t] = -1;  // reset incrementally after each row
   __syncwarp();
@@ -702,37 +650,50 @@ __global__ void __launch_bounds__(SW * 32)
     }
     __syncwarp();
     bool full = false;
-    // (1) s_cc' = a^_cc' for the coarse neighbours of c; collect the F blocks of row c
+    // (1a) the F blocks adjacent to row c: real blocks (1x1 / 2x2 pivots) and the
+    //      virtual blocks of the couplings of adjacent pivot singles (reading R17)
     for (int64_t e = lo + lane; e < hi; e += 32) {
       const int32_t u = col[e];
-      if (!inF[u]) {
-        const int sl = hslot<T>(tab, vals, cmap[u], &scount[wid], list);
-        if (sl < 0)
-          full = true;
-        else
-          vals[sl] = ah[e];
-      } else {
-        const int32_t p = partner[u];
-        bool take = true;
-        double a_cp = 0.0;
-        if (p >= 0) {
-          const int64_t ep = lookup_idx(col, lo, hi, p);
-          if (ep >= 0) a_cp = ah[ep];
-          if (ep >= 0 && p < u) take = false;
+      if (!inF[u]) continue;
+      const int32_t p = partner[u];
+      bool take = true;
+      double a_cp = 0.0;
+      if (p >= 0) {
+        const int64_t ep = lookup_idx(col, lo, hi, p);
+        if (ep >= 0) a_cp = ah[ep];
+        if (ep >= 0 && p < u) take = false;
+      }
+      if (take) {
+        const int bpos = atomicAdd(&sbcount[wid], 1);
+        if (bpos < BM) {
+          BlkEnt bb;
+          if (p < 0) {
+            bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
+            bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
+          } else {
+            bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
+            bb.acf = (bb.f == u) ? ah[e] : a_cp;
+            bb.acg = (bb.g == u) ? ah[e] : a_cp;
+            bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
+          }
+          bb.key = ((int64_t)bb.lead << 32) | (int64_t)bb.lead;
+          blk[bpos] = bb;
         }
-        if (take) {
+      }
+      if (p < 0 && Vptr) {
+        for (int64_t ev = Vptr[u]; ev < Vptr[u + 1]; ++ev) {
+          const int32_t v = Vcol[ev];
+          const int64_t evc = lookup_idx(col, lo, hi, v);
+          if (evc >= 0 && v < u) continue;  // taken at the smaller adjacent member
           const int bpos = atomicAdd(&sbcount[wid], 1);
           if (bpos < BM) {
             BlkEnt bb;
-            if (p < 0) {
-              bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
-              bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
-            } else {
-              bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
-              bb.acf = (bb.f == u) ? ah[e] : a_cp;
-              bb.acg = (bb.g == u) ? ah[e] : a_cp;
-              bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
-            }
+            bb.f = min(u, v); bb.g = max(u, v); bb.lead = bb.f;
+            const double a_cv = (evc >= 0) ? ah[evc] : 0.0;
+            bb.acf = (bb.f == u) ? ah[e] : a_cv;
+            bb.acg = (bb.g == u) ? ah[e] : a_cv;
+            bb.Bff = 0.0; bb.Bgg = 0.0; bb.Bfg = Vval[ev];
+            bb.key = ((int64_t)bb.f << 32) | (int64_t)bb.g;
             blk[bpos] = bb;
           }
         }
@@ -740,64 +701,179 @@ __global__ void __launch_bounds__(SW * 32)
     }
     __syncwarp();
     const int nb = sbcount[wid];
-    if (lane == 0 && nb <= BM) {  // blocks in ascending leader order (insertion sort)
-      for (int a2 = 1; a2 < nb; ++a2) {
-        BlkEnt v = blk[a2];
-        int q = a2 - 1;
-        while (q >= 0 && blk[q].lead > v.lead) {
-          blk[q + 1] = blk[q];
-          --q;
-        }
-        blk[q + 1] = v;
+    // (1b) blocks in ascending key: bitonic sort of (key, index); keys in the free scratch
+    int64_t* skey = reinterpret_cast<int64_t*>(kvals);
+    int32_t* perm = list;
+    int PB = 1;
+    while (PB < nb) PB <<= 1;
+    if (nb <= BM) {
+      for (int t = lane; t < PB; t += 32) {
+        skey[t] = (t < nb) ? blk[t].key : INT64_MAX;
+        perm[t] = t;
       }
+      __syncwarp();
+      for (int kk = 2; kk <= PB; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int t = lane; t < PB; t += 32) {
+            const int ixj = t ^ jj;
+            if (ixj > t) {
+              const int64_t x = skey[t], y = skey[ixj];
+              const bool up = (t & kk) == 0;
+              if ((x > y) == up) {
+                skey[t] = y;
+                skey[ixj] = x;
+                const int32_t tp = perm[t];
+                perm[t] = perm[ixj];
+                perm[ixj] = tp;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int t = lane; t < nb; t += 32) bperm[t] = perm[t];
+      __syncwarp();
+    }
+    // (L) l_cx = sum over blocks (ascending key) of [(a_cf, a_cg) B_b]_x, from 0
+    int lkept = 0;
+    if (nb <= BM) {
+      if (lane == 0) {
+        for (int i = 0; i < nb; ++i) {
+          const BlkEnt& B = blk[bperm[i]];
+          if (B.g < 0) {
+            const int sl = hslot<T>(tab, vals, B.f, &scount[wid], list);
+            if (sl < 0) { full = true; break; }
+            vals[sl] = __dadd_rn(vals[sl], __dmul_rn(B.acf, B.Bff));
+          } else {
+            const int sf = hslot<T>(tab, vals, B.f, &scount[wid], list);
+            if (sf < 0) { full = true; break; }
+            vals[sf] = __dadd_rn(vals[sf], lval_pair(B.acf, B.acg, B.Bff, B.Bfg));
+            const int sg = hslot<T>(tab, vals, B.g, &scount[wid], list);
+            if (sg < 0) { full = true; break; }
+            vals[sg] = __dadd_rn(vals[sg], lval_pair(B.acf, B.acg, B.Bfg, B.Bgg));
+          }
+        }
+      }
+      __syncwarp();
+      // drop the L row, compact the survivors behind the block keys (skey[PB..]) and
+      // their columns (list[2*PB + ...], trailing the slot reads), reset the slots
+      const int nl = min(scount[wid], T);
+      double* lv_out = kvals;
+      int32_t* lc_out = list;
+      for (int t0 = 0; t0 < nl; t0 += 32) {
+        const int t = t0 + lane;
+        bool keep = false;
+        int32_t kk = 0;
+        double vv = 0.0;
+        if (t < nl) {
+          const int32_t sl = lc_out[t];
+          kk = tab[sl];
+          vv = vals[sl];
+          tab[sl] = -1;
+          keep = fabs(vv) >= tau;
+        }
+        __syncwarp();
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int off = lkept + __popc(bal & ((1u << lane) - 1u));
+          lc_out[off] = kk;
+          lv_out[off] = vv;
+        }
+        lkept += __popc(bal);
+        __syncwarp();
+      }
+      if (!__any_sync(0xffffffffu, full)) {
+        unsigned long long lb = 0;
+        if (lane == 0) lb = atomicAdd(lcursor, (unsigned long long)lkept);
+        lb = __shfl_sync(0xffffffffu, lb, 0);
+        if (lane == 0) {
+          lrow_cnt[cp] = lkept;
+          lrow_off[cp] = (int64_t)lb;
+        }
+        if ((int64_t)lb + lkept <= lcap)
+          for (int t = lane; t < lkept; t += 32) {
+            ltmp_col[lb + t] = lc_out[t];
+            ltmp_val[lb + t] = lv_out[t];
+          }
+      }
+      __syncwarp();
+      if (lane == 0) scount[wid] = 0;
+      __syncwarp();
+    }
+    // (1c) s_cc' = a^_cc' for the coarse neighbours of c
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      const int32_t cu = cmap[col[e]];  // -1 on pivots
+      if (cu < 0) continue;
+      const int sl = hslot<T>(tab, vals, cu, &scount[wid], list);
+      if (sl < 0)
+        full = true;
+      else
+        vals[sl] = ah[e];
     }
     __syncwarp();
-    // (2) subtract the block terms, block after block
+    // (2) subtract the block terms: the real blocks in ascending key (they and A^_CC
+    //     define the pattern of the row), then the virtual blocks in ascending key,
+    //     restricted to that pattern -- no fill from the compensation (reading R17)
     if (nb <= BM) {
-      for (int bi = 0; bi < nb && !__any_sync(0xffffffffu, full); ++bi) {
-        const BlkEnt B = blk[bi];
-        if (B.g < 0) {
-          for (int64_t e = ptr[B.f] + lane; e < ptr[B.f + 1]; e += 32) {
-            const int32_t v = col[e];
-            if (inF[v]) continue;
-            const int sl = hslot<T>(tab, vals, cmap[v], &scount[wid], list);
-            if (sl < 0) {
-              full = true;
-              continue;
-            }
-            vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
-          }
-        } else {
-          // rows f and g: entries of f (with a_{c'g} looked up in g), then entries only in g
-          const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
-          for (int pass = 0; pass < 2; ++pass) {
-            const int64_t s0 = pass ? g0 : f0, s1 = pass ? g1 : f1;
-            for (int64_t e = s0 + lane; e < s1; e += 32) {
-              const int32_t v = col[e];
-              if (inF[v]) continue;
-              double a2f, a2g;
-              if (pass == 0) {
-                a2f = ah[e];
-                const int64_t eg = lookup_idx(col, g0, g1, v);
-                a2g = (eg >= 0) ? ah[eg] : 0.0;
-              } else {
-                if (lookup_idx(col, f0, f1, v) >= 0) continue;  // handled in pass 0
-                a2f = 0.0;
-                a2g = ah[e];
-              }
-              const int sl = hslot<T>(tab, vals, cmap[v], &scount[wid], list);
+      for (int vpass = 0; vpass < 2; ++vpass) {
+        for (int bi = 0; bi < nb && !__any_sync(0xffffffffu, full); ++bi) {
+          const BlkEnt B = blk[bperm[bi]];
+          const bool virt = (int32_t)(B.key >> 32) != (int32_t)(B.key & 0xffffffffLL);
+          if (virt != (vpass == 1)) continue;
+          if (B.g < 0) {
+            for (int64_t e = ptr[B.f] + lane; e < ptr[B.f + 1]; e += 32) {
+              const int32_t cv = cmap[col[e]];
+              if (cv < 0) continue;
+              const int sl = hslot<T>(tab, vals, cv, &scount[wid], list);
               if (sl < 0) {
                 full = true;
                 continue;
               }
-              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
-                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
-              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
-              vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
+              vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
+            }
+          } else {
+            // rows f and g: entries of f (with a_{c'g} looked up in g), then entries only
+            // in g.  A virtual block's term B_fg (a_cf a_c'g + a_cg a_c'f) vanishes on the
+            // row whose weight (a_cg for row f, a_cf for row g) is 0: that row is skipped.
+            const bool walk_f = !virt || B.acg != 0.0, walk_g = !virt || B.acf != 0.0;
+            const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
+            for (int pass = 0; pass < 2; ++pass) {
+              if (!(pass ? walk_g : walk_f)) continue;
+              const int64_t s0 = pass ? g0 : f0, s1 = pass ? g1 : f1;
+              for (int64_t e = s0 + lane; e < s1; e += 32) {
+                const int32_t v = col[e];
+                const int32_t cv = cmap[v];
+                if (cv < 0) continue;
+                double a2f, a2g;
+                if (pass == 0) {
+                  a2f = ah[e];
+                  const int64_t eg = walk_g ? lookup_idx(col, g0, g1, v) : -1;
+                  a2g = (eg >= 0) ? ah[eg] : 0.0;
+                } else {
+                  if (walk_f && lookup_idx(col, f0, f1, v) >= 0) continue;  // handled in pass 0
+                  a2f = 0.0;
+                  a2g = ah[e];
+                }
+                int sl;
+                if (virt) {
+                  sl = hfind<T>(tab, cv);
+                  if (sl < 0) continue;  // outside the pattern
+                } else {
+                  sl = hslot<T>(tab, vals, cv, &scount[wid], list);
+                  if (sl < 0) {
+                    full = true;
+                    continue;
+                  }
+                }
+                const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
+                                            __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
+                const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
+                vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
     const int nc = min(scount[wid], T);
@@ -833,6 +909,7 @@ __global__ void __launch_bounds__(SW * 32)
         if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
       } else if (lane == 0) {
         ovf_list[atomicAdd(ovf_count, 1)] = cp;
+        if (nb > BM) atomicAdd(ovf_count + 2, 1);  // diagnostics: block-list overflow
       }
       continue;
     }
@@ -1014,7 +1091,8 @@ __global__ void __launch_bounds__(TB)
                 const double* __restrict__ D, const double* __restrict__ r, const int32_t* __restrict__ partner,
                 const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ LTptr,
                 const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval, const double* __restrict__ zn,
-                double* __restrict__ z) {
+                double* __restrict__ z, const int64_t* __restrict__ Vptr, const int32_t* __restrict__ Vcol,
+                const double* __restrict__ Vval) {
   pdl_launch_dependents();
   if ((int)blockIdx.x >= bF) {
     const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
@@ -1056,6 +1134,8 @@ __global__ void __launch_bounds__(TB)
       }
     }
   }
+  int iv = 0;
+  if (act && Vptr) iv = fidx[fp];
   pdl_wait();
   double acc = 0.0;
   if (act) {
@@ -1063,6 +1143,11 @@ __global__ void __launch_bounds__(TB)
     for (int q = 0; q < PREF; ++q)
       if (pc[q] >= 0) acc += pv[q] * __ldg(&zn[pc[q]]);
     for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)LTval[e] * __ldg(&zn[LTcol[e]]);
+    if (Vptr)  // virtual couplings: -(B~^{-1} - B_d^{-1}) r^_F  (reading R17)
+      for (int64_t e = Vptr[iv] + lane; e < Vptr[iv + 1]; e += G) {
+        const int32_t v = Vcol[e];
+        acc -= Vval[e] * (D[v] * r[v]);
+      }
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1109,11 +1194,13 @@ static void bwd_g(const Level& v, const double* r, const double* zn, double* z, 
   if (v.f32)
     launch_pdl(k_apply_bwd<G, float>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
-               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z);
+               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z,
+               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval);
   else
     launch_pdl(k_apply_bwd<G, double>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
-               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z);
+               (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z,
+               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval);
 }
 
 static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t st) {
@@ -1152,6 +1239,38 @@ __global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __
     for (int j = lane; j < n; j += 32) acc += G[(int64_t)i * n + j] * r[j];
     acc = warp_sum(acc);
     if (lane == 0) z[i] = acc;
+  }
+}
+
+// L rows: gather the per-row runs (forward values scaled by D of the column)
+template <typename TV>
+__global__ void k_l_gather(int nC, const int64_t* __restrict__ Lptr, const int64_t* __restrict__ row_off,
+                           const int32_t* __restrict__ tcol, const double* __restrict__ tval,
+                           const double* __restrict__ D, int32_t* __restrict__ Lcol, TV* __restrict__ Lval,
+                           uint64_t* __restrict__ tkey, double* __restrict__ traw, const int32_t* __restrict__ fmap) {
+  const int lane = threadIdx.x & 31;
+  for (int cp = (blockIdx.x * TB + threadIdx.x) >> 5; cp < nC; cp += (gridDim.x * TB) >> 5) {
+    const int64_t d0 = Lptr[cp], cnt = Lptr[cp + 1] - d0, s0 = row_off[cp];
+    for (int64_t t = lane; t < cnt; t += 32) {
+      const int32_t f = tcol[s0 + t];
+      const double l = tval[s0 + t];
+      Lcol[d0 + t] = f;
+      Lval[d0 + t] = (TV)(l * D[f]);
+      tkey[d0 + t] = ((uint64_t)(uint32_t)fmap[f] << 32) | (uint64_t)(uint32_t)cp;  // transpose key
+      traw[d0 + t] = l;
+    }
+  }
+}
+__global__ void k_lt_count(int64_t nnz, const uint64_t* __restrict__ skey, int64_t* __restrict__ cnt) {
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * TB)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[skey[t] >> 32]), 1ull);
+}
+template <typename TV>
+__global__ void k_lt_fill(int64_t nnz, const uint64_t* __restrict__ skey, const double* __restrict__ sval,
+                          int32_t* __restrict__ LTcol, TV* __restrict__ LTval) {
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * TB) {
+    LTcol[t] = (int32_t)(skey[t] & 0xffffffffull);
+    LTval[t] = (TV)sval[t];
   }
 }
 
@@ -1194,12 +1313,14 @@ void Csr::release(cudaStream_t st) {
 }
 
 void Level::release(cudaStream_t st) {
-  for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)fidx, (void*)partner, (void*)b11, (void*)b12, (void*)Lptr,
-                  (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)r, (void*)z})
+  for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)fidx, (void*)fmap, (void*)partner, (void*)b11, (void*)b12,
+                  (void*)Lptr, (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)Vptr,
+                  (void*)Vcol, (void*)Vval, (void*)r, (void*)z})
     dfree(p, st);
 }
 
 // Factor one level.  Returns false on stall (nothing allocated into lv then).
+static bool verbose_setup();
 static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P, Level& lv, Csr& S,
                          cudaStream_t st) {
   const int n = A.n;
@@ -1323,6 +1444,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
   lv.cidx = dalloc<int32_t>(std::max(nC, 1), st);
   lv.partner = dalloc<int32_t>(n, st);
   lv.fidx = dalloc<int32_t>(std::max(nF, 1), st);
+  lv.fmap = dalloc<int32_t>(n, st);
   {
     int32_t* flag = dalloc<int32_t>(n, st);
     int32_t* scan = dalloc<int32_t>(n, st);
@@ -1330,52 +1452,32 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     AJ_LAUNCHED();
     exclusive_scan_i32(flag, scan, n, st);
     // b11/b12 of C nodes zeroed inside k_cmap (they were block data of non-F nodes)
-    k_cmap<<<g, TB, 0, st>>>(n, inF, scan, lv.cmap, lv.cidx, lv.fidx, lv.partner, partner, b11, b12);
+    k_cmap<<<g, TB, 0, st>>>(n, inF, scan, lv.cmap, lv.cidx, lv.fidx, lv.fmap, lv.partner, partner, b11, b12);
     AJ_LAUNCHED();
     dfree(flag, st);
     dfree(scan, st);
   }
-  // L (forward) rows over coarse nodes
-  {
-    int64_t* cnt = dalloc<int64_t>(std::max(nC, 1), st);
-    const int gc = grid_sg(nC);
-    k_L_rows<false, double><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D,
-                                        P.tau_drop, cnt, nullptr, nullptr);
+  lv.f32 = P.factor_fp32 != 0;
+  // virtual 2x2 blocks of the weak pivot-pivot couplings (reading R17)
+  lv.nnzV = 0;
+  if (P.compensate && latticeL == 0) {
+    int64_t* cnt = dalloc<int64_t>(n, st);
+    k_virtual<false><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, P.tau_virtual, cnt, nullptr, nullptr);
     AJ_LAUNCHED();
-    lv.nnzL = counts_to_ptr(cnt, lv.Lptr, nC, st);
-    lv.Lcol = dalloc<int32_t>(lv.nnzL, st);
-    lv.f32 = P.factor_fp32 != 0;
-    lv.Lval = lv.f32 ? (void*)dalloc<float>(lv.nnzL, st) : (void*)dalloc<double>(lv.nnzL, st);
-    if (lv.f32)
-      k_L_rows<true, float><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D, P.tau_drop,
-                                                lv.Lptr, lv.Lcol, (float*)lv.Lval);
-    else
-      k_L_rows<true, double><<<gc, TB, 0, st>>>(nC, lv.cidx, A.ptr, A.col, ah, inF, partner, b11, b12, D, P.tau_drop,
-                                                 lv.Lptr, lv.Lcol, (double*)lv.Lval);
-    AJ_LAUNCHED();
+    lv.nnzV = counts_to_ptr(cnt, lv.Vptr, n, st);
+    if (lv.nnzV > 0) {
+      lv.Vcol = dalloc<int32_t>(lv.nnzV, st);
+      lv.Vval = dalloc<double>(lv.nnzV, st);
+      k_virtual<true><<<g, TB, 0, st>>>(n, A.ptr, A.col, ah, inF, partner, b11, P.tau_virtual, lv.Vptr, lv.Vcol, lv.Vval);
+      AJ_LAUNCHED();
+    } else {
+      dfree(lv.Vptr, st);
+      lv.Vptr = nullptr;
+    }
     dfree(cnt, st);
   }
-  // L^T (backward) rows over the pivot (F) nodes, in F order
-  {
-    int64_t* cnt = dalloc<int64_t>(nF, st);
-    const int gF = grid_for(nF);
-    k_LT_rows<false, double><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
-                                         P.tau_drop, cnt, nullptr, nullptr);
-    AJ_LAUNCHED();
-    lv.nnzLT = counts_to_ptr(cnt, lv.LTptr, nF, st);
-    lv.LTcol = dalloc<int32_t>(lv.nnzLT, st);
-    lv.LTval = lv.f32 ? (void*)dalloc<float>(lv.nnzLT, st) : (void*)dalloc<double>(lv.nnzLT, st);
-    if (lv.f32)
-      k_LT_rows<true, float><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
-                                                 P.tau_drop, lv.LTptr, lv.LTcol, (float*)lv.LTval);
-    else
-      k_LT_rows<true, double><<<gF, TB, 0, st>>>(nF, lv.fidx, A.ptr, A.col, ah, inF, partner, b11, b12, lv.cmap,
-                                                  P.tau_drop, lv.LTptr, lv.LTcol, (double*)lv.LTval);
-    AJ_LAUNCHED();
-    dfree(cnt, st);
-  }
-  // Schur complement on the coarse nodes: one pass, survivors appended to a temp
-  // buffer through a global cursor, then gathered into CSR order
+  // L rows and the Schur complement on the coarse nodes, one pass: the survivors of
+  // each row are appended to temp buffers through global cursors, then gathered
   {
     S.n = nC;
     const int nwarps_total = std::min(std::max(nC, 1), num_sms() * 8 * SW);
@@ -1384,8 +1486,10 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     int32_t* scr = dalloc<int32_t>((size_t)gs * SW * schur_scratch_words<HT, false>(), st);
     int64_t* row_cnt = dalloc<int64_t>(std::max(nC, 1), st);
     int64_t* row_off = dalloc<int64_t>(std::max(nC, 1), st);
+    int64_t* lrow_cnt = dalloc<int64_t>(std::max(nC, 1), st);
+    int64_t* lrow_off = dalloc<int64_t>(std::max(nC, 1), st);
     int32_t* ovf_list = dalloc<int32_t>(std::max(nC, 1), st);
-    unsigned long long* cursor = dalloc<unsigned long long>(1, st);
+    unsigned long long* cursor = dalloc<unsigned long long>(2, st);
     int* ovf = counters + 5;   // [5] fallback rows, [6] error
     static bool attr_set = false;
     if (!attr_set) {
@@ -1393,50 +1497,101 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
       attr_set = true;
     }
     int64_t cap = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
+    int64_t lcap = std::max<int64_t>((int64_t)nC * 64, 1024);
     int nov = 0;
-    int32_t* tmp_col = nullptr;
-    double* tmp_val = nullptr;
+    int32_t *tmp_col = nullptr, *ltmp_col = nullptr;
+    double *tmp_val = nullptr, *ltmp_val = nullptr;
     int32_t* scrg = nullptr;
     for (int attempt = 0; attempt < 2; ++attempt) {
       tmp_col = dalloc<int32_t>(cap, st);
       tmp_val = dalloc<double>(cap, st);
-      AJ_CUDA(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
-      AJ_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+      ltmp_col = dalloc<int32_t>(lcap, st);
+      ltmp_val = dalloc<double>(lcap, st);
+      AJ_CUDA(cudaMemsetAsync(ovf, 0, 3 * sizeof(int), st));
+      AJ_CUDA(cudaMemsetAsync(cursor, 0, 2 * sizeof(unsigned long long), st));
       k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
-                                                       b11, b12, P.tau_drop, scr, row_cnt, row_off, tmp_col, tmp_val,
-                                                       cap, cursor, ovf_list, ovf, ovf + 1);
+                                                       b11, b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scr, row_cnt,
+                                                       row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off,
+                                                       ltmp_col, ltmp_val, lcap, cursor + 1, ovf_list, ovf, ovf + 1);
       AJ_LAUNCHED();
       nov = read_scalar(ovf, st);
       if (nov > 0) {
         if (!scrg) scrg = dalloc<int32_t>((size_t)gsg2 * SW * schur_scratch_words<HTG, true>(), st);
         k_schur<true><<<gsg2, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
-                                                 b12, P.tau_drop, scrg, row_cnt, row_off, tmp_col, tmp_val, cap,
-                                                 cursor, ovf_list, ovf, ovf + 1);
+                                                 b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scrg, row_cnt, row_off,
+                                                 tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
+                                                 ltmp_val, lcap, cursor + 1, ovf_list, ovf, ovf + 1);
         AJ_LAUNCHED();
         const int err = read_scalar(ovf + 1, st);
         AJ_REQUIRE(err == 0, AJ_ERR_CAPACITY,
                    err == 1 ? "Schur complement: more than 2048 pivot blocks adjacent to one row (raise tau_drop)"
                             : "Schur complement: more than 24576 candidate columns in one row (raise tau_drop)");
       }
-      const int64_t used = (int64_t)read_scalar(cursor, st);
-      if (used <= cap) break;
-      dfree(tmp_col, st);
-      dfree(tmp_val, st);
-      cap = used;  // exact size now known: run again
+      unsigned long long used[2];
+      AJ_CUDA(cudaMemcpyAsync(used, cursor, sizeof(used), cudaMemcpyDeviceToHost, st));
+      AJ_CUDA(cudaStreamSynchronize(st));
+      if ((int64_t)used[0] <= cap && (int64_t)used[1] <= lcap) break;
+      for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val}) dfree(q, st);
+      cap = std::max<int64_t>(cap, (int64_t)used[0]);  // exact sizes now known: run again
+      lcap = std::max<int64_t>(lcap, (int64_t)used[1]);
       AJ_REQUIRE(attempt == 0, AJ_ERR_CAPACITY, "Schur complement: temp capacity");
+      if (verbose_setup())
+        fprintf(stderr, "[aj setup] n=%d: Schur temp capacity retry (S %llu / %lld, L %llu / %lld)\n", n,
+                used[0], (long long)cap, used[1], (long long)lcap);
     }
+    // S in CSR order
     S.nnz = counts_to_ptr(row_cnt, S.ptr, nC, st);
     S.col = dalloc<int32_t>(S.nnz, st);
     S.val = dalloc<double>(S.nnz, st);
-    k_schur_gather<<<std::max(1, std::min(ceil_div((int64_t)nC * 32, TB), num_sms() * 32)), TB, 0, st>>>(
-        nC, S.ptr, row_off, tmp_col, tmp_val, S.col, S.val);
+    const int gg = std::max(1, std::min(ceil_div((int64_t)nC * 32, TB), num_sms() * 32));
+    k_schur_gather<<<gg, TB, 0, st>>>(nC, S.ptr, row_off, tmp_col, tmp_val, S.col, S.val);
     AJ_LAUNCHED();
+    // L (forward rows over coarse nodes, values l*D_f) and L^T (rows over pivots, by sort)
+    lv.nnzL = counts_to_ptr(lrow_cnt, lv.Lptr, nC, st);
+    lv.nnzLT = lv.nnzL;
+    const int64_t nL = std::max<int64_t>(lv.nnzL, 1);
+    lv.Lcol = dalloc<int32_t>(nL, st);
+    lv.Lval = lv.f32 ? (void*)dalloc<float>(nL, st) : (void*)dalloc<double>(nL, st);
+    uint64_t* tkey = dalloc<uint64_t>(nL, st);
+    uint64_t* tkey2 = dalloc<uint64_t>(nL, st);
+    double* traw = dalloc<double>(nL, st);
+    double* traw2 = dalloc<double>(nL, st);
+    if (lv.f32)
+      k_l_gather<float><<<gg, TB, 0, st>>>(nC, lv.Lptr, lrow_off, ltmp_col, ltmp_val, D, lv.Lcol, (float*)lv.Lval,
+                                            tkey, traw, lv.fmap);
+    else
+      k_l_gather<double><<<gg, TB, 0, st>>>(nC, lv.Lptr, lrow_off, ltmp_col, ltmp_val, D, lv.Lcol, (double*)lv.Lval,
+                                             tkey, traw, lv.fmap);
+    AJ_LAUNCHED();
+    {
+      size_t tmpb = 0;
+      AJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, tkey, tkey2, traw, traw2, (int)lv.nnzL, 0, 64, st));
+      void* tb = dalloc<char>(tmpb, st);
+      AJ_CUDA(cub::DeviceRadixSort::SortPairs(tb, tmpb, tkey, tkey2, traw, traw2, (int)lv.nnzL, 0, 64, st));
+      dfree(tb, st);
+      int64_t* cntF = dalloc<int64_t>(std::max(nF, 1), st);
+      AJ_CUDA(cudaMemsetAsync(cntF, 0, sizeof(int64_t) * std::max(nF, 1), st));
+      const int gl = std::max(1, std::min(grid_for(lv.nnzL), num_sms() * 32));
+      k_lt_count<<<gl, TB, 0, st>>>(lv.nnzL, tkey2, cntF);
+      AJ_LAUNCHED();
+      const int64_t chk = counts_to_ptr(cntF, lv.LTptr, nF, st);
+      AJ_REQUIRE(chk == lv.nnzL, AJ_ERR_CUDA, "L transpose count mismatch");
+      lv.LTcol = dalloc<int32_t>(nL, st);
+      lv.LTval = lv.f32 ? (void*)dalloc<float>(nL, st) : (void*)dalloc<double>(nL, st);
+      if (lv.f32)
+        k_lt_fill<float><<<gl, TB, 0, st>>>(lv.nnzL, tkey2, traw2, lv.LTcol, (float*)lv.LTval);
+      else
+        k_lt_fill<double><<<gl, TB, 0, st>>>(lv.nnzL, tkey2, traw2, lv.LTcol, (double*)lv.LTval);
+      AJ_LAUNCHED();
+      dfree(cntF, st);
+    }
+    for (void* q : {(void*)tkey, (void*)tkey2, (void*)traw, (void*)traw2}) dfree(q, st);
     if (scrg) dfree(scrg, st);
-    dfree(tmp_col, st);
-    dfree(tmp_val, st);
-    dfree(cursor, st);
-    dfree(row_off, st);
+    for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val, (void*)cursor, (void*)row_off,
+                    (void*)lrow_off, (void*)lrow_cnt})
+      dfree(q, st);
     lv.schur_fallback_rows = nov;
+    lv.schur_fallback_nb = nov > 0 ? read_scalar(ovf + 2, st) : 0;
     dfree(scr, st);
     dfree(ovf_list, st);
     dfree(row_cnt, st);
@@ -1463,13 +1618,16 @@ static double wall_ms() {
 }
 
 // Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 min(1, (50/L)^2),
-// tau_strong = 10 tau_drop (R12; the paper scales its drop tolerance with the size too,
+// tau_strong = min(0.05, 40 tau_drop) with compensation (R17), else 10 tau_drop,
+// tau_virtual = 5 tau_drop (R12; the paper scales its drop tolerance with the size too,
 // eps = 1/sqrt(N)).
 aj_precond_params resolve_params(const aj_precond_params& in, int L) {
   aj_precond_params P = in;
   const double sc = (50.0 / L) * (50.0 / L);
   if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
-  if (P.tau_strong < 0.0) P.tau_strong = 10.0 * P.tau_drop;
+  if (P.tau_strong < 0.0) P.tau_strong = P.compensate ? std::min(0.05, 40.0 * P.tau_drop) : 10.0 * P.tau_drop;
+  if (P.tau_virtual < 0.0) P.tau_virtual = 5.0 * P.tau_drop;
+  if (!P.compensate) P.tau_virtual = 0.0;
   if (P.max_levels > 1023) P.max_levels = 1023;
   return P;
 }
@@ -1510,9 +1668,11 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
       if (verbose_setup()) {
         AJ_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "[aj setup] level %d n=%d nF=%d pairs=%d mis_rounds=%d nnzA=%lld nnzS=%lld nnzL=%lld %.2f ms\n", lev,
-                lv.n, lv.nF, lv.npairs, lv.rounds, (long long)A.nnz, (long long)S.nnz, (long long)lv.nnzL,
-                wall_ms() - t0);
+        fprintf(stderr,
+                "[aj setup] level %d n=%d nF=%d pairs=%d virt=%lld mis_rounds=%d nnzA=%lld nnzS=%lld nnzL=%lld "
+                "fallback_rows=%d (blocks %d) %.2f ms\n",
+                lev, lv.n, lv.nF, lv.npairs, (long long)lv.nnzV / 2, lv.rounds, (long long)A.nnz, (long long)S.nnz,
+                (long long)lv.nnzL, lv.schur_fallback_rows, lv.schur_fallback_nb, wall_ms() - t0);
       }
       if (lev > 0) {
         lv.r = dalloc<double>(lv.n, st);
@@ -1580,6 +1740,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   for (size_t l = 0; l < K->lv.size(); ++l) {
     const Level& v = K->lv[l];
     I.nnz_L += v.nnzL;
+    I.nnz_V += v.nnzV / 2;
     I.level_n[l] = v.n;
     I.level_nF[l] = v.nF;
     I.level_pairs[l] = v.npairs;
@@ -1588,6 +1749,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   I.setup_ms = ms;
   I.tau_drop = P.tau_drop;
   I.tau_strong = P.tau_strong;
+  I.tau_virtual = P.tau_virtual;
   K->bytes_per_apply = precond_bytes_per_apply(K);
   precond_capture(K, st);
   prepare_tail(K, st);
@@ -1750,6 +1912,8 @@ static void prepare_tail(Precond* K, cudaStream_t st) {
   const char* e = getenv("AJ_TAIL");
   if (!(e && atoi(e) == 1)) return;
   if (K->P.factor_fp32) return;  // the cooperative path reads fp64 factors only
+  for (const auto& v : K->lv)
+    if (v.nnzV > 0) return;      // ... and has no virtual couplings
   if (K->lv.size() < 2) return;
   std::vector<LevelDesc> h(K->lv.size());
   for (size_t l = 0; l < K->lv.size(); ++l) {
@@ -1816,7 +1980,7 @@ int64_t precond_bytes_per_apply(const Precond* K) {
   // (8 B value + 4 B index) plus per-level vectors (r read twice, D, z/rn writes)
   int64_t b = 0;
   for (const auto& v : K->lv) {
-    b += (v.nnzL + v.nnzLT) * (v.f32 ? 8 : 12);
+    b += (v.nnzL + v.nnzLT) * (v.f32 ? 8 : 12) + v.nnzV * 12;
     b += (int64_t)v.n * (8 /*D*/ + 8 /*r*/ + 8 /*z*/ + 4 /*cmap*/ + 8 * 2 /*b11,b12 for F*/ + 4 /*partner*/);
     b += (int64_t)v.nC * (4 + 8 + 8 + 8);  // cidx, D_c r_c, rn write, L ptr
   }

@@ -16,12 +16,13 @@ struct Csr {
 };
 
 struct Level {
-  int n = 0, nF = 0, nC = 0, npairs = 0, rounds = 0, schur_fallback_rows = 0;
+  int n = 0, nF = 0, nC = 0, npairs = 0, rounds = 0, schur_fallback_rows = 0, schur_fallback_nb = 0;
   int64_t nnzL = 0, nnzLT = 0, nnzS = 0;
   double* D = nullptr;          // n   symmetric scaling of this level
   int32_t* cmap = nullptr;      // n   coarse index of C nodes, -1 for F
   int32_t* cidx = nullptr;      // nC  level index of coarse node c'
   int32_t* fidx = nullptr;      // nF  level index of pivot node f'
+  int32_t* fmap = nullptr;      // n   pivot index of F nodes, -1 for C
   int32_t* partner = nullptr;   // n   2x2 partner of F nodes, else -1
   double* b11 = nullptr;        // n   B^{-1}[f,f]   (F nodes)
   double* b12 = nullptr;        // n   B^{-1}[f,g]   (F nodes of a pair)
@@ -32,6 +33,10 @@ struct Level {
   int32_t* LTcol = nullptr;     // coarse index
   void* LTval = nullptr;        // L_cf        (float if f32, else double)
   bool f32 = false;             // factor values stored in fp32 (accumulation stays fp64)
+  int64_t* Vptr = nullptr;      // n+1 virtual couplings of pivot singles (reading R17)
+  int32_t* Vcol = nullptr;      // level index of the coupled pivot
+  double* Vval = nullptr;       // b'_uv
+  int64_t nnzV = 0;
   int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;

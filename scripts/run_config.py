@@ -28,8 +28,12 @@ def main():
     eps = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
     binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
     jp = binding.default_jd_params(verbose=1, max_outer=int(os.environ.get("AJ_MAX_OUTER", "600")))
+    pp = binding.default_precond_params()
+    for key, env in (("tau_drop", "AJ_TD"), ("tau_strong", "AJ_TS"), ("tau_virtual", "AJ_TV")):
+        if env in os.environ:
+            setattr(pp, key, float(os.environ[env]))
     t0 = time.perf_counter()
-    lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], jparams=jp)
+    lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     normA = 6 * abs(cfg["hop"]) + float(eps.abs().max())
@@ -38,6 +42,7 @@ def main():
                solve_ms=st["solve_ms"], outer=st["outer"], inner=st["inner_total"],
                levels=st["precond"]["levels"], coarse=st["precond"]["coarse_n"],
                tau_drop=st["precond"]["tau_drop"], tau_strong=st["precond"]["tau_strong"],
+               tau_virtual=st["precond"]["tau_virtual"], nnz_V=st["precond"]["nnz_V"],
                nnzL_per_site=st["precond"]["nnz_L"] / L ** 3, eigenvalues=[float(v) for v in lam],
                resid_rel=[float(v) / normA for v in res], orth_err=float(np.abs(G - np.eye(len(lam))).max()))
     print(json.dumps(out), flush=True)

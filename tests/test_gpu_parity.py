@@ -82,7 +82,10 @@ def test_spmv_plane_wave_gpu(gpu_lib):
 def resolved(p, L):
     """DESIGN.md R12 auto rule for negative drop parameters."""
     td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
-    ts = p.tau_strong if p.tau_strong >= 0 else 10 * td
+    if p.tau_strong >= 0:
+        ts = p.tau_strong
+    else:
+        ts = min(0.05, 40 * td) if p.compensate else 10 * td
     return td, ts
 
 
@@ -91,16 +94,17 @@ def _oracle_precond(L, eps, hop, sigma, p):
     td, ts = resolved(p, L)
     return mlildl.MultilevelILDL(A, lattice_L=L, kappa=p.kappa, tau_drop=td, tau_strong=ts,
                                  n_coarse_max=p.n_coarse_max, max_levels=p.max_levels, stall_frac=p.stall_frac,
-                                 dense_cap=p.dense_cap, factor_fp32=bool(p.factor_fp32))
+                                 dense_cap=p.dense_cap, factor_fp32=bool(p.factor_fp32),
+                                 compensate=bool(p.compensate))
 
 
-@pytest.mark.parametrize("fp32", [1, 0])
+@pytest.mark.parametrize("fp32,comp", [(0, 1), (1, 1), (0, 0)])
 @pytest.mark.parametrize("L,W,seed,hop,sigma", [(8, 16.5, 1, -1.0, 0.0), (12, 16.5, 2, -1.0, 0.0),
                                                 (16, 12.0, 3, 1.0, 0.25), (11, 21.0, 4, -1.0, 0.0),
-                                                (20, 16.5, 5, -1.0, 0.0)])
-def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32):
+                                                (20, 16.5, 5, -1.0, 0.0), (24, 16.5, 6, -1.0, 0.0)])
+def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
     import torch
-    p = gpu_lib.default_precond_params(n_coarse_max=200, factor_fp32=fp32)
+    p = gpu_lib.default_precond_params(n_coarse_max=200, factor_fp32=fp32, compensate=comp)
     eps_g = gpu_eps(gpu_lib, L, W, seed)
     K = gpu_lib.Precond(eps_g, L, hop, sigma, p)
     info = K.info()

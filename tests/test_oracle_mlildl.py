@@ -162,3 +162,36 @@ def test_fp32_factor_storage_close_to_fp64():
     b = np.random.default_rng(5).standard_normal(L ** 3)
     x, it, res, _ = sqmr(lambda v: A @ v, M32.apply, b, tol=1e-10, maxit=150)
     assert res <= 1e-10
+
+
+def test_weak_coupling_compensation_by_hand():
+    # reading R17: pivots 0 and 1 are weakly coupled (e < tau_strong) and both
+    # strongly coupled to node 2.  B = [[1, e], [e, 1]] is replaced by its first-order
+    # inverse I - E, so S = 1 - (a^2 + b^2 - 2 a b e) and L = (a - b e, b - a e);
+    # without compensation the e terms are lost.
+    a, b, e = 0.5, 0.6, 0.01
+    A = sp.csr_matrix(np.array([[1.0, e, a], [e, 1.0, b], [a, b, 1.0]]))
+    Lv = mlildl.factor_level(A, kappa=5.0, tau_drop=0.0, tau_strong=0.02)
+    assert list(Lv.F) == [0, 1] and Lv.nvirtual == 1
+    assert np.isclose(Lv.S.toarray()[0, 0], 1.0 - (a * a + b * b - 2 * a * b * e), rtol=0, atol=1e-15)
+    assert np.allclose(Lv.L.toarray()[0, :2], [a - b * e, b - a * e], rtol=0, atol=1e-15)
+    exact = 1.0 - np.array([a, b]) @ np.linalg.solve(np.array([[1.0, e], [e, 1.0]]), np.array([a, b]))
+    assert abs(Lv.S.toarray()[0, 0] - exact) < 2 * e * e
+    L0 = mlildl.factor_level(A, kappa=5.0, tau_drop=0.0, tau_strong=0.02, compensate=False)
+    assert L0.nvirtual == 0
+    assert np.isclose(L0.S.toarray()[0, 0], 1.0 - (a * a + b * b), atol=1e-15)
+
+
+def test_compensation_improves_preconditioner():
+    # at a coarse strong threshold the compensated factor needs fewer SQMR steps
+    L = 16
+    A = an.matrix(L, an.disorder(L, 16.5, 2), hop=-1.0)
+    b = np.random.default_rng(5).standard_normal(L ** 3)
+    its = {}
+    for comp in (False, True):
+        M = mlildl.MultilevelILDL(A, lattice_L=L, tau_drop=2e-3, tau_strong=0.05, n_coarse_max=300,
+                                  compensate=comp)
+        x, it, res, _ = sqmr(lambda v: A @ v, M.apply, b, tol=1e-8, maxit=500)
+        assert res <= 1e-8
+        its[comp] = it
+    assert its[True] < its[False]

@@ -514,6 +514,10 @@ __global__ void k_virtual(int n, const int64_t* __restrict__ ptr, const int32_t*
   }
 }
 
+__global__ void k_iota(int n, int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) out[i] = i;
+}
+
 constexpr int SW = 4;            // warps per CTA
 constexpr int BMAX = 1024;       // F blocks (real + virtual) adjacent to one row (shared-memory variant)
 constexpr int HT = 2048;         // per-warp hash table, shared-memory variant (power of 2)
@@ -556,12 +560,16 @@ __device__ __forceinline__ void warp_bitonic_sort_kv(int32_t* a, double* v, int 
   }
 }
 
-// find-or-insert `key` into a warp's table of size T (power of 2); returns the
-// slot or -1 when full.  New keys get value 0 and their slot appended to `list`.
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+// find-or-insert `key` into a table of size T (power of 2); returns the slot, or
+// -1 once the table holds 3T/4 keys (the row is then handed to the next tier; the
+// load cap keeps probe chains short).  New keys get value 0 and their slot
+// appended to `list`.
 template <int T>
 __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int* cnt, int32_t* list) {
-  constexpr int BITS = (T == 2048) ? 11 : 15;
-  static_assert(T == 2048 || T == 32768, "table size");
+  constexpr int BITS = ilog2c(T);
+  static_assert((T & (T - 1)) == 0, "table size");
   uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
   for (int probe = 0; probe < T; ++probe) {
     const int32_t prev = atomicCAS(&tab[h], -1, key);
@@ -569,7 +577,7 @@ __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int
       val[h] = 0.0;
       const int pos = atomicAdd(cnt, 1);
       if (pos < T) list[pos] = (int32_t)h;
-      return (int)h;
+      return pos < (T * 3) / 4 ? (int)h : -1;
     }
     if (prev == key) return (int)h;
     h = (h + 1) & (T - 1);
@@ -580,7 +588,7 @@ __device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int
 // slot of `key` in a warp's table, or -1 if absent (no insertion)
 template <int T>
 __device__ __forceinline__ int hfind(const int32_t* tab, int32_t key) {
-  constexpr int BITS = (T == 2048) ? 11 : 15;
+  constexpr int BITS = ilog2c(T);
   uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
   for (int probe = 0; probe < T; ++probe) {
     const int32_t k = tab[h];
@@ -909,7 +917,6 @@ __global__ void __launch_bounds__(SW * 32, 2)
         if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
       } else if (lane == 0) {
         ovf_list[atomicAdd(ovf_count, 1)] = cp;
-        if (nb > BM) atomicAdd(ovf_count + 2, 1);  // diagnostics: block-list overflow
       }
       continue;
     }
@@ -937,6 +944,345 @@ __global__ void __launch_bounds__(SW * 32, 2)
     __syncwarp();
     for (int t = lane; t < P; t += 32) tab[t] = -1;  // the table is empty again
     __syncwarp();
+  }
+}
+
+// CTA-per-row variant of k_schur for the rows the warp variant cannot hold (more
+// than 3/4 HT candidates): the same arithmetic in the same per-entry order, one
+// CTA of CT threads per row, the table (HTC entries) in shared memory.  The block
+// terms are applied block after block with a barrier in between; each coarse
+// neighbour c' appears at most once per block, so threads never share a slot
+// inside a block.  Rows that still do not fit are queued to ovf_list.
+constexpr int CT = 256;
+constexpr int HTC = 16384;
+constexpr int BMAXC = 2048;
+constexpr size_t kSchurCtaSmem = (size_t)HTC * (sizeof(int32_t) + sizeof(double));
+constexpr size_t schur_cta_scratch_words() { return (size_t)HTC * 4 + (size_t)BMAXC * (sizeof(BlkEnt) / 4 + 1); }
+
+__device__ __forceinline__ void cta_bitonic_sort_kv(int32_t* a, double* v, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < P; t += CT) {
+        const int ixj = t ^ j;
+        if (ixj > t) {
+          const int32_t x = a[t], y = a[ixj];
+          const bool up = (t & k) == 0;
+          if ((x > y) == up) {
+            a[t] = y;
+            a[ixj] = x;
+            const double tv = v[t];
+            v[t] = v[ixj];
+            v[ixj] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(CT, 1)
+    k_schur_cta(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
+                const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
+                const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ Vptr,
+                const int32_t* __restrict__ Vcol, const double* __restrict__ Vval, double tau,
+                int32_t* __restrict__ scratch_all, int64_t* __restrict__ row_cnt, int64_t* __restrict__ row_off,
+                int32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, int64_t cap,
+                unsigned long long* __restrict__ cursor, int64_t* __restrict__ lrow_cnt,
+                int64_t* __restrict__ lrow_off, int32_t* __restrict__ ltmp_col, double* __restrict__ ltmp_val,
+                int64_t lcap, unsigned long long* __restrict__ lcursor, int32_t* __restrict__ ovf_list,
+                int* __restrict__ ovf_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int scount, sbcount, sfull, skept;
+  __shared__ unsigned long long sbase;
+  double* vals = reinterpret_cast<double*>(smem_raw);
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)HTC * sizeof(double));
+  const int tid = threadIdx.x, lane = tid & 31;
+  int32_t* wscr = scratch_all + (size_t)blockIdx.x * schur_cta_scratch_words();
+  int32_t* list = wscr;                                          // HTC int32 (slot list)
+  double* kvals = reinterpret_cast<double*>(wscr + HTC);         // HTC doubles
+  int32_t* keys2 = wscr + 3 * HTC;                               // HTC int32
+  BlkEnt* blk = reinterpret_cast<BlkEnt*>(wscr + 4 * HTC);
+  int32_t* bperm = wscr + 4 * HTC + (size_t)BMAXC * (sizeof(BlkEnt) / 4);
+  for (int t = tid; t < HTC; t += CT) tab[t] = -1;
+  __syncthreads();
+  for (int ri = blockIdx.x; ri < nrows; ri += gridDim.x) {
+    const int cp = rowlist[ri];
+    const int c = cidx[cp];
+    const int64_t lo = ptr[c], hi = ptr[c + 1];
+    if (tid == 0) {
+      scount = 0;
+      sbcount = 0;
+      sfull = 0;
+      skept = 0;
+    }
+    __syncthreads();
+    // (1a) real and virtual blocks adjacent to row c (as in k_schur)
+    for (int64_t e = lo + tid; e < hi; e += CT) {
+      const int32_t u = col[e];
+      if (!inF[u]) continue;
+      const int32_t p = partner[u];
+      bool take = true;
+      double a_cp = 0.0;
+      if (p >= 0) {
+        const int64_t ep = lookup_idx(col, lo, hi, p);
+        if (ep >= 0) a_cp = ah[ep];
+        if (ep >= 0 && p < u) take = false;
+      }
+      if (take) {
+        const int bpos = atomicAdd(&sbcount, 1);
+        if (bpos < BMAXC) {
+          BlkEnt bb;
+          if (p < 0) {
+            bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
+            bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
+          } else {
+            bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
+            bb.acf = (bb.f == u) ? ah[e] : a_cp;
+            bb.acg = (bb.g == u) ? ah[e] : a_cp;
+            bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
+          }
+          bb.key = ((int64_t)bb.lead << 32) | (int64_t)bb.lead;
+          blk[bpos] = bb;
+        }
+      }
+      if (p < 0 && Vptr) {
+        for (int64_t ev = Vptr[u]; ev < Vptr[u + 1]; ++ev) {
+          const int32_t v = Vcol[ev];
+          const int64_t evc = lookup_idx(col, lo, hi, v);
+          if (evc >= 0 && v < u) continue;
+          const int bpos = atomicAdd(&sbcount, 1);
+          if (bpos < BMAXC) {
+            BlkEnt bb;
+            bb.f = min(u, v); bb.g = max(u, v); bb.lead = bb.f;
+            const double a_cv = (evc >= 0) ? ah[evc] : 0.0;
+            bb.acf = (bb.f == u) ? ah[e] : a_cv;
+            bb.acg = (bb.g == u) ? ah[e] : a_cv;
+            bb.Bff = 0.0; bb.Bgg = 0.0; bb.Bfg = Vval[ev];
+            bb.key = ((int64_t)bb.f << 32) | (int64_t)bb.g;
+            blk[bpos] = bb;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nb = sbcount;
+    bool bad = nb > BMAXC;
+    if (!bad) {
+      // (1b) ascending block key
+      int64_t* skey = reinterpret_cast<int64_t*>(kvals);
+      int32_t* perm = list;
+      int PB = 1;
+      while (PB < nb) PB <<= 1;
+      for (int t = tid; t < PB; t += CT) {
+        skey[t] = (t < nb) ? blk[t].key : INT64_MAX;
+        perm[t] = t;
+      }
+      __syncthreads();
+      for (int kk = 2; kk <= PB; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int t = tid; t < PB; t += CT) {
+            const int ixj = t ^ jj;
+            if (ixj > t) {
+              const int64_t x = skey[t], y = skey[ixj];
+              const bool up = (t & kk) == 0;
+              if ((x > y) == up) {
+                skey[t] = y;
+                skey[ixj] = x;
+                const int32_t tp = perm[t];
+                perm[t] = perm[ixj];
+                perm[ixj] = tp;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int t = tid; t < nb; t += CT) bperm[t] = perm[t];
+      __syncthreads();
+      // (L) sequential accumulation in ascending key (thread 0), then warp 0 drops,
+      //     compacts and emits the row of L
+      if (tid == 0) {
+        for (int i = 0; i < nb; ++i) {
+          const BlkEnt& B = blk[bperm[i]];
+          if (B.g < 0) {
+            const int sl = hslot<HTC>(tab, vals, B.f, &scount, list);
+            if (sl < 0) { sfull = 1; break; }
+            vals[sl] = __dadd_rn(vals[sl], __dmul_rn(B.acf, B.Bff));
+          } else {
+            const int sf = hslot<HTC>(tab, vals, B.f, &scount, list);
+            if (sf < 0) { sfull = 1; break; }
+            vals[sf] = __dadd_rn(vals[sf], lval_pair(B.acf, B.acg, B.Bff, B.Bfg));
+            const int sg = hslot<HTC>(tab, vals, B.g, &scount, list);
+            if (sg < 0) { sfull = 1; break; }
+            vals[sg] = __dadd_rn(vals[sg], lval_pair(B.acf, B.acg, B.Bfg, B.Bgg));
+          }
+        }
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const int nl = min(scount, HTC);
+        int lkept = 0;
+        for (int t0 = 0; t0 < nl; t0 += 32) {
+          const int t = t0 + lane;
+          bool keep = false;
+          int32_t kk = 0;
+          double vv = 0.0;
+          if (t < nl) {
+            const int32_t sl = list[t];
+            kk = tab[sl];
+            vv = vals[sl];
+            tab[sl] = -1;
+            keep = fabs(vv) >= tau;
+          }
+          __syncwarp();
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int off = lkept + __popc(bal & ((1u << lane) - 1u));
+            list[off] = kk;
+            kvals[off] = vv;
+          }
+          lkept += __popc(bal);
+          __syncwarp();
+        }
+        if (!sfull) {
+          unsigned long long lb = 0;
+          if (lane == 0) lb = atomicAdd(lcursor, (unsigned long long)lkept);
+          lb = __shfl_sync(0xffffffffu, lb, 0);
+          if (lane == 0) {
+            lrow_cnt[cp] = lkept;
+            lrow_off[cp] = (int64_t)lb;
+          }
+          if ((int64_t)lb + lkept <= lcap)
+            for (int t = lane; t < lkept; t += 32) {
+              ltmp_col[lb + t] = list[t];
+              ltmp_val[lb + t] = kvals[t];
+            }
+        }
+        if (lane == 0) scount = 0;
+      }
+      __syncthreads();
+    }
+    // (1c) s_cc' = a^_cc'
+    for (int64_t e = lo + tid; e < hi; e += CT) {
+      const int32_t cu = cmap[col[e]];
+      if (cu < 0) continue;
+      const int sl = hslot<HTC>(tab, vals, cu, &scount, list);
+      if (sl < 0)
+        sfull = 1;
+      else
+        vals[sl] = ah[e];
+    }
+    __syncthreads();
+    // (2) real blocks, then virtual blocks on the pattern (as in k_schur)
+    bool full_any = sfull != 0;  // uniform: read after the barrier; sfull is not written below
+    if (!bad && !full_any) {
+      bool lfull = false;
+      for (int vpass = 0; vpass < 2 && !full_any; ++vpass) {
+        for (int bi = 0; bi < nb; ++bi) {
+          const BlkEnt B = blk[bperm[bi]];
+          const bool virt = (int32_t)(B.key >> 32) != (int32_t)(B.key & 0xffffffffLL);
+          if (virt != (vpass == 1)) continue;
+          if (B.g < 0) {
+            for (int64_t e = ptr[B.f] + tid; e < ptr[B.f + 1]; e += CT) {
+              const int32_t cv = cmap[col[e]];
+              if (cv < 0) continue;
+              const int sl = hslot<HTC>(tab, vals, cv, &scount, list);
+              if (sl < 0) {
+                lfull = true;
+                continue;
+              }
+              vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
+            }
+          } else {
+            const bool walk_f = !virt || B.acg != 0.0, walk_g = !virt || B.acf != 0.0;
+            const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
+            const int64_t nf = walk_f ? f1 - f0 : 0, ng = walk_g ? g1 - g0 : 0;
+            for (int64_t q = tid; q < nf + ng; q += CT) {
+              const bool pass = q >= nf;
+              const int64_t e = pass ? g0 + (q - nf) : f0 + q;
+              const int32_t v = col[e];
+              const int32_t cv = cmap[v];
+              if (cv < 0) continue;
+              double a2f, a2g;
+              if (!pass) {
+                a2f = ah[e];
+                const int64_t eg = walk_g ? lookup_idx(col, g0, g1, v) : -1;
+                a2g = (eg >= 0) ? ah[eg] : 0.0;
+              } else {
+                if (walk_f && lookup_idx(col, f0, f1, v) >= 0) continue;
+                a2f = 0.0;
+                a2g = ah[e];
+              }
+              int sl;
+              if (virt) {
+                sl = hfind<HTC>(tab, cv);
+                if (sl < 0) continue;
+              } else {
+                sl = hslot<HTC>(tab, vals, cv, &scount, list);
+                if (sl < 0) {
+                  lfull = true;
+                  continue;
+                }
+              }
+              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
+                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
+              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
+              vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
+            }
+          }
+          if (__syncthreads_or(lfull)) {
+            full_any = true;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nc = min(scount, HTC);
+    bad = bad || full_any || scount > (HTC * 3) / 4;
+    // (3) collect through the slot list, reset the slots, drop; survivors in any order
+    for (int t = tid; t < nc; t += CT) {
+      const int32_t sl = list[t];
+      const int32_t kk = tab[sl];
+      const double vv = vals[sl];
+      tab[sl] = -1;
+      if (!bad && ((kk == cp) || (fabs(vv) >= tau))) {
+        const int off = atomicAdd(&skept, 1);
+        keys2[off] = kk;
+        kvals[off] = vv;
+      }
+    }
+    __syncthreads();
+    if (bad) {
+      if (tid == 0) ovf_list[atomicAdd(ovf_count, 1)] = cp;
+      continue;  // uniform
+    }
+    const int kept = skept;
+    int P = 1;
+    while (P < kept) P <<= 1;
+    for (int t = tid; t < P; t += CT) {
+      tab[t] = (t < kept) ? keys2[t] : INT32_MAX;
+      vals[t] = (t < kept) ? kvals[t] : 0.0;
+    }
+    __syncthreads();
+    cta_bitonic_sort_kv(tab, vals, P);
+    if (tid == 0) {
+      sbase = atomicAdd(cursor, (unsigned long long)kept);
+      row_cnt[cp] = kept;
+      row_off[cp] = (int64_t)sbase;
+    }
+    __syncthreads();
+    const unsigned long long base = sbase;
+    if ((int64_t)base + kept <= cap)
+      for (int t = tid; t < kept; t += CT) {
+        tmp_col[base + t] = tab[t];
+        tmp_val[base + t] = vals[t];
+      }
+    __syncthreads();
+    for (int t = tid; t < P; t += CT) tab[t] = -1;
+    __syncthreads();
   }
 }
 
@@ -1482,7 +1828,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     S.n = nC;
     const int nwarps_total = std::min(std::max(nC, 1), num_sms() * 8 * SW);
     const int gs = std::max(1, ceil_div(nwarps_total, SW));
-    const int gsg2 = std::min(gs, num_sms());  // fallback grid (large global tables)
+    const int gsg2 = std::min(gs, num_sms());  // fallback grids (large tables)
     int32_t* scr = dalloc<int32_t>((size_t)gs * SW * schur_scratch_words<HT, false>(), st);
     int64_t* row_cnt = dalloc<int64_t>(std::max(nC, 1), st);
     int64_t* row_off = dalloc<int64_t>(std::max(nC, 1), st);
@@ -1494,8 +1840,11 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     static bool attr_set = false;
     if (!attr_set) {
       AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurCtaSmem));
       attr_set = true;
     }
+    int32_t* ovf2_list = nullptr;
+    int32_t* scrc = nullptr;
     int64_t cap = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
     int64_t lcap = std::max<int64_t>((int64_t)nC * 64, 1024);
     int nov = 0;
@@ -1509,15 +1858,44 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
       ltmp_val = dalloc<double>(lcap, st);
       AJ_CUDA(cudaMemsetAsync(ovf, 0, 3 * sizeof(int), st));
       AJ_CUDA(cudaMemsetAsync(cursor, 0, 2 * sizeof(unsigned long long), st));
-      k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner,
-                                                       b11, b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scr, row_cnt,
-                                                       row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off,
-                                                       ltmp_col, ltmp_val, lcap, cursor + 1, ovf_list, ovf, ovf + 1);
-      AJ_LAUNCHED();
-      nov = read_scalar(ovf, st);
-      if (nov > 0) {
+      // AJ_SCHUR_TIER=2/3 (testing): start every row at the CTA / global-table variant
+      const char* ftier = getenv("AJ_SCHUR_TIER");
+      const int first_tier = ftier ? atoi(ftier) : 1;
+      if (first_tier <= 1) {
+        k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
+                                                         partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scr,
+                                                         row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt,
+                                                         lrow_off, ltmp_col, ltmp_val, lcap, cursor + 1, ovf_list, ovf,
+                                                         ovf + 1);
+        AJ_LAUNCHED();
+        nov = read_scalar(ovf, st);
+      } else {
+        nov = nC;
+        k_iota<<<g, TB, 0, st>>>(nC, ovf_list);
+        AJ_LAUNCHED();
+      }
+      int nov2 = 0;
+      if (nov > 0 && first_tier >= 3) {
+        nov2 = nov;
+        if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
+        k_iota<<<g, TB, 0, st>>>(nC, ovf2_list);
+        AJ_LAUNCHED();
+      } else if (nov > 0) {
+        // tier 2: one CTA per row, 16384-entry shared-memory table
+        if (!scrc) scrc = dalloc<int32_t>((size_t)gsg2 * schur_cta_scratch_words(), st);
+        if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
+        AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
+        k_schur_cta<<<std::min(nov, gsg2), CT, kSchurCtaSmem, st>>>(
+            nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
+            P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
+            ltmp_val, lcap, cursor + 1, ovf2_list, ovf + 2);
+        AJ_LAUNCHED();
+        nov2 = read_scalar(ovf + 2, st);
+      }
+      if (nov2 > 0) {
+        // tier 3: one warp per row, 32768-entry tables in global memory
         if (!scrg) scrg = dalloc<int32_t>((size_t)gsg2 * SW * schur_scratch_words<HTG, true>(), st);
-        k_schur<true><<<gsg2, SW * 32, 0, st>>>(nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
+        k_schur<true><<<gsg2, SW * 32, 0, st>>>(nov2, ovf2_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
                                                  b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scrg, row_cnt, row_off,
                                                  tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
                                                  ltmp_val, lcap, cursor + 1, ovf_list, ovf, ovf + 1);
@@ -1587,6 +1965,8 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     }
     for (void* q : {(void*)tkey, (void*)tkey2, (void*)traw, (void*)traw2}) dfree(q, st);
     if (scrg) dfree(scrg, st);
+    if (scrc) dfree(scrc, st);
+    if (ovf2_list) dfree(ovf2_list, st);
     for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val, (void*)cursor, (void*)row_off,
                     (void*)lrow_off, (void*)lrow_cnt})
       dfree(q, st);
@@ -1670,7 +2050,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
         AJ_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "[aj setup] level %d n=%d nF=%d pairs=%d virt=%lld mis_rounds=%d nnzA=%lld nnzS=%lld nnzL=%lld "
-                "fallback_rows=%d (blocks %d) %.2f ms\n",
+                "fallback_rows=%d (tier3 %d) %.2f ms\n",
                 lev, lv.n, lv.nF, lv.npairs, (long long)lv.nnzV / 2, lv.rounds, (long long)A.nnz, (long long)S.nnz,
                 (long long)lv.nnzL, lv.schur_fallback_rows, lv.schur_fallback_nb, wall_ms() - t0);
       }

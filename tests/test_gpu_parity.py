@@ -118,6 +118,9 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
     assert info["level_pairs"] == [lv.npairs for lv in M.levels]
     assert info["coarse_n"] == M.coarse_n
     assert info["level_nnzS"] == [lv.S.nnz for lv in M.levels]
+    assert info["nnz_L"] == sum(lv.L.nnz for lv in M.levels)
+    assert info["nnz_V"] == sum(lv.nvirtual for lv in M.levels)
+    assert info["tau_virtual"] == (5.0 * info["tau_drop"] if comp else 0.0)
     for s in (21, 22):
         r = rand_vec(L ** 3, s)
         z = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
@@ -125,6 +128,31 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
         zr = M.apply(r)
         assert np.linalg.norm(N(z) - zr) <= 1e-8 * np.linalg.norm(zr)
     K.free()
+
+
+@pytest.mark.parametrize("tier", [2, 3])
+def test_precond_schur_tiers_agree(gpu_lib, monkeypatch, tier):
+    # the CTA-per-row (tier 2) and global-table (tier 3) Schur variants compute the
+    # same level structure and the same factor, bit for bit, as the warp variant
+    import torch
+    L = 16
+    p = gpu_lib.default_precond_params(n_coarse_max=200)
+    eps_g = gpu_eps(gpu_lib, L, 16.5, 5)
+    r = T(rand_vec(L ** 3, 4))
+    K1 = gpu_lib.Precond(eps_g, L, -1.0, 0.0, p)
+    z1 = torch.empty_like(r)
+    K1.apply(z1, r)
+    i1 = K1.info()
+    K1.free()
+    monkeypatch.setenv("AJ_SCHUR_TIER", str(tier))
+    K2 = gpu_lib.Precond(eps_g, L, -1.0, 0.0, p)
+    z2 = torch.empty_like(r)
+    K2.apply(z2, r)
+    i2 = K2.info()
+    K2.free()
+    for key in ("levels", "level_n", "level_nF", "level_pairs", "level_nnzS", "nnz_L", "nnz_V", "coarse_n"):
+        assert i1[key] == i2[key], key
+    assert torch.equal(z1, z2)
 
 
 def test_precond_exactness_limit_gpu(gpu_lib):

@@ -87,7 +87,8 @@ typedef struct {
   int32_t compensate;    /* 1: first-order treatment of the dropped weak pivot-pivot
                             couplings, B^{-1} ~ B_d^{-1} - B_d^{-1} E B_d^{-1} (R17) */
   double tau_virtual;    /* only couplings |a^_uv| >= tau_virtual are compensated;
-                            < 0: auto, 5 * tau_drop (R17)                           */
+                            < 0: auto, 5 tau_drop (L <= 50) .. 10 tau_drop
+                            (L >= 100), linear in between                        */
 } aj_precond_params;
 
 typedef struct {

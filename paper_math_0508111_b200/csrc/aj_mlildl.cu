@@ -821,23 +821,38 @@ __global__ void __launch_bounds__(SW * 32, 2)
     __syncwarp();
     // (2) subtract the block terms: the real blocks in ascending key (they and A^_CC
     //     define the pattern of the row), then the virtual blocks in ascending key,
-    //     restricted to that pattern -- no fill from the compensation (reading R17)
+    //     restricted to that pattern -- no fill from the compensation (reading R17).
+    //     Each lane gathers SU entries of a block row before hashing them (ILP).
     if (nb <= BM) {
+      constexpr int SU = 4;
       for (int vpass = 0; vpass < 2; ++vpass) {
         for (int bi = 0; bi < nb && !__any_sync(0xffffffffu, full); ++bi) {
           const BlkEnt B = blk[bperm[bi]];
           const bool virt = (int32_t)(B.key >> 32) != (int32_t)(B.key & 0xffffffffLL);
           if (virt != (vpass == 1)) continue;
           if (B.g < 0) {
-            for (int64_t e = ptr[B.f] + lane; e < ptr[B.f + 1]; e += 32) {
-              const int32_t cv = cmap[col[e]];
-              if (cv < 0) continue;
-              const int sl = hslot<T>(tab, vals, cv, &scount[wid], list);
-              if (sl < 0) {
-                full = true;
-                continue;
+            const int64_t r0 = ptr[B.f], r1 = ptr[B.f + 1];
+            for (int64_t e0 = r0 + lane; e0 < r1; e0 += 32 * SU) {
+              int32_t cv[SU];
+              double av[SU];
+#pragma unroll
+              for (int u = 0; u < SU; ++u) {
+                const int64_t e = e0 + 32 * u;
+                cv[u] = (e < r1) ? col[e] : -1;
+                av[u] = (e < r1) ? ah[e] : 0.0;
               }
-              vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
+#pragma unroll
+              for (int u = 0; u < SU; ++u) cv[u] = (cv[u] >= 0) ? cmap[cv[u]] : -1;
+#pragma unroll
+              for (int u = 0; u < SU; ++u) {
+                if (cv[u] < 0) continue;
+                const int sl = hslot<T>(tab, vals, cv[u], &scount[wid], list);
+                if (sl < 0) {
+                  full = true;
+                  continue;
+                }
+                vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, av[u])));
+              }
             }
           } else {
             // rows f and g: entries of f (with a_{c'g} looked up in g), then entries only
@@ -845,29 +860,39 @@ __global__ void __launch_bounds__(SW * 32, 2)
             // row whose weight (a_cg for row f, a_cf for row g) is 0: that row is skipped.
             const bool walk_f = !virt || B.acg != 0.0, walk_g = !virt || B.acf != 0.0;
             const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
-            for (int pass = 0; pass < 2; ++pass) {
-              if (!(pass ? walk_g : walk_f)) continue;
-              const int64_t s0 = pass ? g0 : f0, s1 = pass ? g1 : f1;
-              for (int64_t e = s0 + lane; e < s1; e += 32) {
-                const int32_t v = col[e];
-                const int32_t cv = cmap[v];
-                if (cv < 0) continue;
+            const int64_t nf = walk_f ? f1 - f0 : 0, ntot = nf + (walk_g ? g1 - g0 : 0);
+            for (int64_t q0 = lane; q0 < ntot; q0 += 32 * SU) {
+              int32_t vv[SU], cv[SU];
+              double av[SU];
+#pragma unroll
+              for (int u = 0; u < SU; ++u) {
+                const int64_t q = q0 + 32 * u;
+                const int64_t e = (q < nf) ? f0 + q : g0 + (q - nf);
+                vv[u] = (q < ntot) ? col[e] : -1;
+                av[u] = (q < ntot) ? ah[e] : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < SU; ++u) cv[u] = (vv[u] >= 0) ? cmap[vv[u]] : -1;
+#pragma unroll
+              for (int u = 0; u < SU; ++u) {
+                if (cv[u] < 0) continue;
+                const bool pass = (q0 + 32 * u) >= nf;
                 double a2f, a2g;
-                if (pass == 0) {
-                  a2f = ah[e];
-                  const int64_t eg = walk_g ? lookup_idx(col, g0, g1, v) : -1;
+                if (!pass) {
+                  a2f = av[u];
+                  const int64_t eg = walk_g ? lookup_idx(col, g0, g1, vv[u]) : -1;
                   a2g = (eg >= 0) ? ah[eg] : 0.0;
                 } else {
-                  if (walk_f && lookup_idx(col, f0, f1, v) >= 0) continue;  // handled in pass 0
+                  if (walk_f && lookup_idx(col, f0, f1, vv[u]) >= 0) continue;  // handled with row f
                   a2f = 0.0;
-                  a2g = ah[e];
+                  a2g = av[u];
                 }
                 int sl;
                 if (virt) {
-                  sl = hfind<T>(tab, cv);
+                  sl = hfind<T>(tab, cv[u]);
                   if (sl < 0) continue;  // outside the pattern
                 } else {
-                  sl = hslot<T>(tab, vals, cv, &scount[wid], list);
+                  sl = hslot<T>(tab, vals, cv[u], &scount[wid], list);
                   if (sl < 0) {
                     full = true;
                     continue;
@@ -1999,14 +2024,15 @@ static double wall_ms() {
 
 // Resolve "auto" (negative) drop parameters: tau_drop = 2e-3 min(1, (50/L)^2),
 // tau_strong = min(0.05, 40 tau_drop) with compensation (R17), else 10 tau_drop,
-// tau_virtual = 5 tau_drop (R12; the paper scales its drop tolerance with the size too,
+// tau_virtual = 5..10 tau_drop (L = 50..100) (R12; the paper scales its drop tolerance with the size too,
 // eps = 1/sqrt(N)).
 aj_precond_params resolve_params(const aj_precond_params& in, int L) {
   aj_precond_params P = in;
   const double sc = (50.0 / L) * (50.0 / L);
   if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
   if (P.tau_strong < 0.0) P.tau_strong = P.compensate ? std::min(0.05, 40.0 * P.tau_drop) : 10.0 * P.tau_drop;
-  if (P.tau_virtual < 0.0) P.tau_virtual = 5.0 * P.tau_drop;
+  if (P.tau_virtual < 0.0)  // 5 tau_drop up to L = 50, 10 tau_drop from L = 100 (measured, R17)
+    P.tau_virtual = std::min(10.0, std::max(5.0, 5.0 + 5.0 * (L - 50) / 50.0)) * P.tau_drop;
   if (!P.compensate) P.tau_virtual = 0.0;
   if (P.max_levels > 1023) P.max_levels = 1023;
   return P;

@@ -27,8 +27,10 @@ level matrix A_l (symmetric, explicit diagonal):
  (iii) Factor: L = A^_CF B^{-1} (entries < tau_drop dropped, the paper's
       "drop these entries whenever their absolute value is less than
       eps/kappa", l.909-911), S = A^_CC - A^_CF B^{-1} A^_FC symmetrised and
-      off-diagonals < tau_drop dropped (reading R10), F-F couplings (all weak
-      by construction of the independent set) are dropped.
+      off-diagonals < tau_drop dropped (reading R10).  F-F couplings (all weak
+      by construction of the independent set) are dropped, or, with
+      compensate=True (reading R17), those >= tau_virtual enter B^{-1} to first
+      order as virtual 2x2 blocks (in L with fill, in S on the pattern only).
  (iv) Recursion on S (sect. 7.3, l.917-945) until n <= n_coarse_max, the level
       cap, or a level eliminates < stall_frac*n nodes; the last Schur
       complement is inverted densely.

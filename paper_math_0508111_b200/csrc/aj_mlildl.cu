@@ -1521,7 +1521,17 @@ __global__ void __launch_bounds__(TB)
       }
   }
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int o = (G < 32 ? G : 32) / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if constexpr (G > 32) {  // long rows (deep levels): G / 32 warps per row, fixed-order sum
+    __shared__ double part[TB / 32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (lane == 0) {
+      acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < G / 32; ++k) acc += part[(threadIdx.x >> 5) + k];
+    }
+  }
   if (act && lane == 0) {
     double y = B1 * (Di * r[i]);
     if (p >= 0) y += B2 * (Dp * r[p]);
@@ -1529,9 +1539,9 @@ __global__ void __launch_bounds__(TB)
   }
 }
 
-static int pick_group(double avg_len) {
+static int pick_group(double avg_len, int gmax = 32) {
   int g = 1;
-  while (g < 32 && g * 2 <= avg_len) g <<= 1;  // ~2 entries per lane
+  while (g < gmax && g * 2 <= avg_len) g <<= 1;  // ~2 entries per lane
   return g;
 }
 
@@ -1595,7 +1605,10 @@ static void launch_bwd(const Level& v, const double* r, const double* zn, double
     case 4: bwd_g<4>(v, r, zn, z, bF, grid, st); break;
     case 8: bwd_g<8>(v, r, zn, z, bF, grid, st); break;
     case 16: bwd_g<16>(v, r, zn, z, bF, grid, st); break;
-    default: bwd_g<32>(v, r, zn, z, bF, grid, st); break;
+    case 32: bwd_g<32>(v, r, zn, z, bF, grid, st); break;
+    case 64: bwd_g<64>(v, r, zn, z, bF, grid, st); break;
+    case 128: bwd_g<128>(v, r, zn, z, bF, grid, st); break;
+    default: bwd_g<256>(v, r, zn, z, bF, grid, st); break;
   }
 }
 
@@ -2085,7 +2098,9 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
         lv.z = dalloc<double>(lv.n, st);
       }
       lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0);
-      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0);
+      // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
+      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0, lv.nF <= 2048 ? TB : 32);
+      if (const char* fg = getenv("AJ_FORCE_GB")) lv.gb = atoi(fg);    // testing: every backward group size
       K->lv.push_back(lv);
       A.release(st);
       A = S;

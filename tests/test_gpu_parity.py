@@ -155,6 +155,28 @@ def test_precond_schur_tiers_agree(gpu_lib, monkeypatch, tier):
     assert torch.equal(z1, z2)
 
 
+def test_precond_backward_group_sizes_agree(gpu_lib, monkeypatch):
+    # the backward kernel's row-group size (1 lane ... a whole CTA per L^T row) only
+    # changes the summation order
+    import torch
+    L = 16
+    eps_g = gpu_eps(gpu_lib, L, 16.5, 7)
+    r = T(rand_vec(L ** 3, 6))
+    zs = {}
+    for gb in (None, 1, 32, 64, 128, 256):
+        if gb is None:
+            monkeypatch.delenv("AJ_FORCE_GB", raising=False)
+        else:
+            monkeypatch.setenv("AJ_FORCE_GB", str(gb))
+        K = gpu_lib.Precond(eps_g, L, -1.0, 0.0, gpu_lib.default_precond_params(n_coarse_max=200))
+        z = torch.empty_like(r)
+        K.apply(z, r)
+        K.free()
+        zs[gb] = z
+    for gb, z in zs.items():
+        assert torch.linalg.norm(z - zs[None]) <= 1e-13 * torch.linalg.norm(zs[None]), gb
+
+
 def test_precond_exactness_limit_gpu(gpu_lib):
     # no dropping, no kappa bound, true independent sets -> K^{-1} = (A - sigma I)^{-1}
     import torch

@@ -1413,7 +1413,7 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-constexpr int PREF = 4;  // factor entries per lane prefetched before the dependency wait
+constexpr int PREF = 8;  // factor entries per lane prefetched before the dependency wait
 
 template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
@@ -1539,9 +1539,14 @@ __global__ void __launch_bounds__(TB)
   }
 }
 
-static int pick_group(double avg_len, int gmax = 32) {
+// G lanes per row such that each lane holds ~per_lane entries: 8 on large levels
+// (streaming, more loads in flight per thread), 4 on small L2-resident ones (more
+// threads); measured at L = 50..200 (DESIGN.md sect. 4)
+static int pick_group(double avg_len, int64_t nnz, int gmax = 32) {
+  static const char* ev = getenv("AJ_PER_LANE");
+  const int per_lane = ev ? atoi(ev) : (nnz > (int64_t(1) << 22) ? 8 : 4);
   int g = 1;
-  while (g < gmax && g * 2 <= avg_len) g <<= 1;  // ~2 entries per lane
+  while (g < gmax && g * per_lane <= avg_len) g <<= 1;  // ~per_lane entries per lane (memory-level parallelism)
   return g;
 }
 
@@ -2097,9 +2102,9 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
         lv.r = dalloc<double>(lv.n, st);
         lv.z = dalloc<double>(lv.n, st);
       }
-      lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0);
+      lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0, lv.nnzL);
       // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
-      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0, lv.nF <= 2048 ? TB : 32);
+      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0, lv.nnzLT, lv.nF <= 2048 ? TB : 32);
       if (const char* fg = getenv("AJ_FORCE_GB")) lv.gb = atoi(fg);    // testing: every backward group size
       K->lv.push_back(lv);
       A.release(st);

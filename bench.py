@@ -34,7 +34,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--big-L", type=int, default=250, help="lattice for the SpMV/precond HBM roofline pass (0=off)")
+    ap.add_argument("--big-L", type=int, default=250, help="lattice for the SpMV HBM roofline pass (0=off)")
+    ap.add_argument("--precond-L", type=int, default=150,
+                    help="lattice for the preconditioner-apply roofline pass, production parameters (0=off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     # tuning knobs (defaults = library defaults, aj_*_default_params)
@@ -204,8 +206,9 @@ def workload_config(cfg):
             "parallelism": "independent disorder realisations per rank (seed + rank)"}
 
 
-def big_roofline(binding, L, peak):
-    """SpMV and preconditioner-apply HBM throughput at a lattice larger than L2."""
+def big_roofline(binding, L, peak, Lp):
+    """SpMV (lattice L) and preconditioner-apply (lattice Lp, production parameters)
+    HBM throughput, both working sets far larger than L2."""
     import torch
     out = {"L": L, "n": L ** 3}
     n = L ** 3
@@ -226,12 +229,21 @@ def big_roofline(binding, L, peak):
     ms = e0.elapsed_time(e1) / reps
     gbs = 24.0 * n / (ms * 1e-3) / 1e9
     out["spmv"] = {"ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_site": 24}
+    del eps, x, y
+    torch.cuda.empty_cache()
+    if Lp <= 0:
+        return out
+    n = Lp ** 3
+    eps = torch.empty(n, dtype=torch.float64, device="cuda")
+    binding.anderson_build(eps, Lp, 16.5, 4)
+    x = torch.randn(n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
     try:
         t0 = time.perf_counter()
-        # kernel-throughput pass: factor with the fixed L=50 production drop parameters so the
-        # pass stays bounded (the size-scaled defaults of R12 take minutes to factor at L=250)
-        pp = binding.default_precond_params(tau_drop=2e-3, tau_strong=2e-2)
-        K = binding.Precond(eps, L, -1.0, 0.0, pp)
+        # production (auto, size-scaled) parameters of DESIGN.md R12/R17; the factor of
+        # L=150 (7 GB per apply) is far larger than L2
+        pp = binding.default_precond_params()
+        K = binding.Precond(eps, Lp, -1.0, 0.0, pp)
         torch.cuda.synchronize()
         out["precond_setup_s"] = time.perf_counter() - t0
         info = K.info()
@@ -249,7 +261,7 @@ def big_roofline(binding, L, peak):
         ms = e0.elapsed_time(e1) / reps
         by = prof["precond_apply"]["bytes"] / max(1, prof["precond_apply"]["calls"])
         gbs = by / (ms * 1e-3) / 1e9
-        out["precond_apply"] = {"ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_apply": by,
+        out["precond_apply"] = {"L": Lp, "ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_apply": by,
                                 "levels": info["levels"], "coarse_n": info["coarse_n"],
                                 "nnz_L_per_site": info["nnz_L"] / n, "tau_drop": info["tau_drop"],
                                 "tau_strong": info["tau_strong"]}
@@ -357,7 +369,7 @@ def run_ours(args, cfg, ws, rank, local):
     if rank == 0 and args.big_L and ws == 1:
         try:
             log(f"kernel roofline pass at L={args.big_L}")
-            kr = big_roofline(binding, args.big_L, peak)
+            kr = big_roofline(binding, args.big_L, peak, args.precond_L)
         except Exception as ex:
             kr = {"error": str(ex)[:300]}
 

@@ -1,0 +1,4 @@
+# parity + apply timing at L=50..250
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "precond" > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
+for L in 50 100 150 200; do timeout 600 python scripts/prof_kernels.py $L 10 precond > gpurun_out/ap$L.log 2>&1; echo "$(tail -1 gpurun_out/ap$L.log)"; done

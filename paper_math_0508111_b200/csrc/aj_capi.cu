@@ -211,7 +211,7 @@ void aj_jd_default_params(aj_jd_params* p) {
   p->jmin = 10;
   p->jmax = 25;
   p->max_outer = 2000;
-  p->inner_max = 60;
+  p->inner_max = 150;   // DESIGN.md R15: measured vs 60 at L=50..250, W=16.5 and 21
   p->inner_tol = 3e-3;
   p->switch_tol = 1e-3;
   p->seed = 7;

@@ -2089,7 +2089,15 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       Level lv;
       Csr S;
       const double t0 = verbose_setup() ? wall_ms() : 0.0;
-      if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
+      aj_precond_params Pl = P;
+      {  // experimental (AJ_ROWCAP=r): raise tau_drop on levels whose matrix exceeds r entries per row
+        static const char* rc = getenv("AJ_ROWCAP");
+        if (rc && A.n > 0) {
+          const double avg = (double)A.nnz / A.n, cap = atof(rc);
+          if (avg > cap) Pl.tau_drop = P.tau_drop * (avg / cap);
+        }
+      }
+      if (!factor_level(A, lev == 0 ? L : 0, Pl, lv, S, st)) break;
       if (verbose_setup()) {
         AJ_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,

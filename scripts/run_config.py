@@ -28,6 +28,10 @@ def main():
     eps = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
     binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
     jp = binding.default_jd_params(verbose=1, max_outer=int(os.environ.get("AJ_MAX_OUTER", "600")))
+    if "AJ_INNER_MAX" in os.environ:
+        jp.inner_max = int(os.environ["AJ_INNER_MAX"])
+    if "AJ_INNER_TOL" in os.environ:
+        jp.inner_tol = float(os.environ["AJ_INNER_TOL"])
     pp = binding.default_precond_params()
     for key, env in (("tau_drop", "AJ_TD"), ("tau_strong", "AJ_TS"), ("tau_virtual", "AJ_TV")):
         if env in os.environ:

@@ -206,6 +206,17 @@ def workload_config(cfg):
             "parallelism": "independent disorder realisations per rank (seed + rank)"}
 
 
+def apply_traffic(L):
+    """DRAM bytes of one preconditioner apply at lattice L from the committed ncu capture
+    (profiles/round1_apply_traffic.json, written by scripts/apply_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round1_apply_traffic.json")) as f:
+            t = json.load(f)
+        return float(t[str(L)]["dram_bytes"])
+    except Exception:
+        return None
+
+
 def big_roofline(binding, L, peak, Lp):
     """SpMV (lattice L) and preconditioner-apply (lattice Lp, production parameters)
     HBM throughput, both working sets far larger than L2."""
@@ -262,6 +273,7 @@ def big_roofline(binding, L, peak, Lp):
         by = prof["precond_apply"]["bytes"] / max(1, prof["precond_apply"]["calls"])
         gbs = by / (ms * 1e-3) / 1e9
         out["precond_apply"] = {"L": Lp, "ms": ms, "GB/s": gbs, "frac": gbs / peak, "bytes_per_apply": by,
+                                "traffic": apply_traffic(Lp),
                                 "levels": info["levels"], "coarse_n": info["coarse_n"],
                                 "nnz_L_per_site": info["nnz_L"] / n, "tau_drop": info["tau_drop"],
                                 "tau_strong": info["tau_strong"]}
@@ -333,7 +345,10 @@ def run_ours(args, cfg, ws, rank, local):
     avg_ms = d["ms"] / d["calls"]
     achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "frac": achieved / peak,
+            "traffic": apply_traffic(L) if dom == "precond_apply" else None,
+            "traffic_source": "profiles/round1_apply_traffic.json (ncu dram__bytes_read+write, one apply)",
+            "peak_source": peak_src,
             "avg_launch_ms": avg_ms, "bytes_per_launch": d["bytes"] / d["calls"],
             "share_of_step": d["ms"] / total_ms,
             "phases": {c: {"ms_per_step": v["ms"] / args.steps, "calls_per_step": v["calls"] / args.steps,

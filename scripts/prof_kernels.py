@@ -1,7 +1,7 @@
 """Kernel-level driver for ncu / timing: disorder, stencil SpMV and one
 preconditioner setup + applies at lattice size L (default 250).
 
-python scripts/prof_kernels.py [L] [reps] [what]   what in {spmv, precond, all}
+python scripts/prof_kernels.py [L] [reps] [what] [seed]   what in {spmv, precond, all}
 """
 import os
 import sys
@@ -17,9 +17,10 @@ def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 250
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     what = sys.argv[3] if len(sys.argv) > 3 else "all"
+    seed = int(sys.argv[4]) if len(sys.argv) > 4 else 4
     n = L ** 3
     eps = torch.empty(n, dtype=torch.float64, device="cuda")
-    binding.anderson_build(eps, L, 16.5, 4)
+    binding.anderson_build(eps, L, 16.5, seed)
     x = torch.randn(n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
     st = torch.cuda.current_stream()

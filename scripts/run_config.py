@@ -36,6 +36,8 @@ def main():
     for key, env in (("tau_drop", "AJ_TD"), ("tau_strong", "AJ_TS"), ("tau_virtual", "AJ_TV")):
         if env in os.environ:
             setattr(pp, key, float(os.environ[env]))
+    if "AJ_DENSE_CAP" in os.environ:
+        pp.dense_cap = int(os.environ["AJ_DENSE_CAP"])
     t0 = time.perf_counter()
     lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp)
     torch.cuda.synchronize()

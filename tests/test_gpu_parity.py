@@ -384,6 +384,26 @@ def test_jd_config2_l100_properties(gpu_lib):
     assert np.allclose(np.sort(lam1), np.sort(lam2), atol=1e-10 * normA)
 
 
+def test_jd_config3_l200_properties(gpu_lib):
+    # BASELINE configs[3] at full size (n = 8*10^6) on one GPU: residuals recomputed with
+    # the oracle stencil (north-star bounds: ||Ax - lambda x|| <= 1e-8 ||A||), Rayleigh
+    # quotients, orthonormality, eigenvalues inside the Gershgorin interval near sigma
+    cfg = CONFIGS[3]
+    L, W, seed, hop, k = cfg["L"], cfg["W"], cfg["seed"], cfg["hop"], cfg["k"]
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    e = an.disorder(L, W, seed)
+    normA = 6 + np.abs(e).max()
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop)
+    Xh = N(X)
+    for i in range(k):
+        ax = an.stencil_apply(L, e, Xh[:, i], hop=hop)
+        assert np.linalg.norm(ax - lam[i] * Xh[:, i]) <= 1e-8 * normA
+        assert abs(Xh[:, i] @ ax - lam[i]) <= 1e-10 * normA
+        assert res[i] <= 1e-8 * normA
+    assert np.abs(Xh.T @ Xh - np.eye(k)).max() <= 1e-8
+    assert np.abs(lam).max() < 1e-3   # interior: the level spacing near 0 at n = 8e6 is ~1e-6
+
+
 def test_sqmr_graph_path_agrees(gpu_lib, monkeypatch):
     # the optional captured SQMR step (AJ_SQMR_GRAPH=1) runs the same arithmetic
     import torch

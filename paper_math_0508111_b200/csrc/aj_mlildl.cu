@@ -1387,11 +1387,14 @@ __global__ void k_gj_pivot(int n, int k, double* __restrict__ M, double* __restr
 }
 __global__ void k_gj_elim(int n, int k, double* __restrict__ M, const double* __restrict__ fcol) {
   const int64_t w = 2 * (int64_t)n;
-  // rows i != k: M[i, :] -= f_i * M[k, :]
-  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * w; t += (int64_t)gridDim.x * TB) {
-    const int64_t i = t / w, j = t % w;
-    const double f = fcol[i];
-    if (f != 0.0) M[t] -= f * M[(int64_t)k * w + j];
+  // rows i != k: M[i, j] -= f_i * M[k, j] for j > k (columns <= k are never read again)
+  for (int i = blockIdx.y; i < n; i += gridDim.y) {
+    const double f = fcol[i];  // 0 for i == k
+    if (f == 0.0) continue;
+    double* Mi = M + (int64_t)i * w;
+    const double* Mk = M + (int64_t)k * w;
+    for (int64_t j = k + 1 + blockIdx.x * (int64_t)TB + threadIdx.x; j < w; j += (int64_t)gridDim.x * TB)
+      Mi[j] -= f * Mk[j];
   }
 }
 __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __restrict__ G) {
@@ -2137,10 +2140,14 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       AJ_LAUNCHED();
       k_dense_scatter<<<grid_for(nc), TB, 0, st>>>(nc, A.ptr, A.col, A.val, M);
       AJ_LAUNCHED();
+      // one (pivot, eliminate) launch pair per column; the elimination touches only the
+      // columns j > k that are still read (left part) or returned (right part)
+      const int gy = std::min(nc, 1024);
       for (int k = 0; k < nc; ++k) {
         k_gj_pivot<<<1, TB, 0, st>>>(nc, k, M, fcol, sing);
         AJ_LAUNCHED();
-        k_gj_elim<<<gd, TB, 0, st>>>(nc, k, M, fcol);
+        const int gx = std::max(1, std::min(ceil_div(2 * nc - k - 1, TB), 8));
+        k_gj_elim<<<dim3(gx, gy), TB, 0, st>>>(nc, k, M, fcol);
         AJ_LAUNCHED();
       }
       AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");

@@ -1397,6 +1397,160 @@ __global__ void k_gj_elim(int n, int k, double* __restrict__ M, const double* __
       Mi[j] -= f * Mk[j];
   }
 }
+// Gauss-Jordan with implicit row pivoting, one launch per column (the default):
+// the rows are never swapped; prow holds the scaled pivot row of step k.  Step k
+// eliminates column k from every row but the pivot row, records each CTA's best
+// candidate for column k+1 among the rows not yet pivoted (largest |a|, smallest
+// row on ties -- the rule of k_gj_pivot), and the last CTA to finish picks the next
+// pivot row, scales it and stages it in prow for step k+1.  Per element the
+// arithmetic is that of k_gj_pivot + k_gj_elim.
+struct GjState {
+  int* prow_idx;        // pivot row of each step (n)
+  int8_t* pivoted;      // row already used as a pivot (n)
+  double* prow;         // 2 x 2n staged, scaled pivot rows (double buffer)
+  double* pv;           // per-CTA candidate |a|
+  int* pi;              // per-CTA candidate row
+  unsigned int* count;  // CTAs finished in the current step
+  int* singular;
+};
+
+__device__ void gj_pick_and_stage(int n, int k1, double* __restrict__ M, GjState S, int nparts) {
+  // one CTA (TB threads): reduce the candidates for column k1 (largest |a|, smallest
+  // row on ties), scale the pivot row, stage it
+  __shared__ double rv[TB];
+  __shared__ int ri[TB];
+  __shared__ int s_p;
+  __shared__ double s_inv;
+  const int64_t w = 2 * (int64_t)n;
+  double bb = -1.0;
+  int bp = n;
+  for (int c = threadIdx.x; c < nparts; c += TB) {
+    const double v = __ldcg(&S.pv[c]);
+    const int ix = __ldcg(&S.pi[c]);
+    if (v > bb || (v == bb && ix < bp)) {
+      bb = v;
+      bp = ix;
+    }
+  }
+  rv[threadIdx.x] = bb;
+  ri[threadIdx.x] = bp;
+  __syncthreads();
+  for (int s2 = TB / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2 &&
+        (rv[threadIdx.x + s2] > rv[threadIdx.x] || (rv[threadIdx.x + s2] == rv[threadIdx.x] && ri[threadIdx.x + s2] < ri[threadIdx.x]))) {
+      rv[threadIdx.x] = rv[threadIdx.x + s2];
+      ri[threadIdx.x] = ri[threadIdx.x + s2];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bb = rv[0];
+    bp = ri[0];
+    if (!(bb > 0.0) || bp >= n) {
+      *S.singular = 1;
+      bp = -1;
+    } else {
+      S.prow_idx[k1] = bp;
+      S.pivoted[bp] = 1;
+      s_inv = 1.0 / __ldcg(&M[(int64_t)bp * w + k1]);
+    }
+    s_p = bp;
+  }
+  __syncthreads();
+  const int p = s_p;
+  if (p < 0) return;
+  const double inv = s_inv;
+  double* pr = S.prow + (int64_t)(k1 & 1) * w;
+  for (int64_t j = k1 + threadIdx.x; j < w; j += blockDim.x) {
+    const double v = __ldcg(&M[(int64_t)p * w + j]) * inv;
+    M[(int64_t)p * w + j] = v;
+    pr[j] = v;
+  }
+}
+
+__global__ void k_gj_first(int n, double* __restrict__ M, GjState S) {
+  // candidates for column 0 over all rows, then pick/stage (single CTA)
+  __shared__ double sv[TB];
+  __shared__ int si[TB];
+  const int64_t w = 2 * (int64_t)n;
+  double best = -1.0;
+  int bi = n;
+  for (int i = threadIdx.x; i < n; i += TB) {
+    const double a = fabs(M[(int64_t)i * w]);
+    if (a > best) {
+      best = a;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s2 = TB / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2 &&
+        (sv[threadIdx.x + s2] > sv[threadIdx.x] || (sv[threadIdx.x + s2] == sv[threadIdx.x] && si[threadIdx.x + s2] < si[threadIdx.x]))) {
+      sv[threadIdx.x] = sv[threadIdx.x + s2];
+      si[threadIdx.x] = si[threadIdx.x + s2];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S.pv[0] = sv[0];
+    S.pi[0] = si[0];
+  }
+  __threadfence_block();
+  __syncthreads();
+  gj_pick_and_stage(n, 0, M, S, 1);
+}
+
+__global__ void __launch_bounds__(TB) k_gj_step(int n, int k, double* __restrict__ M, GjState S) {
+  __shared__ bool s_last;
+  if (*(volatile int*)S.singular) return;  // a previous step found no pivot
+  const int64_t w = 2 * (int64_t)n;
+  const int p = S.prow_idx[k];
+  const double* pr = S.prow + (int64_t)(k & 1) * w;
+  const bool next = k + 1 < n;
+  double best = -1.0;  // this CTA's candidate for column k+1 (kept by thread 0)
+  int bi = n;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    double* Mi = M + (int64_t)i * w;
+    if (i != p) {
+      const double f = Mi[k];
+      if (f != 0.0)
+        for (int64_t j = k + 1 + threadIdx.x; j < w; j += TB) Mi[j] -= f * pr[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && next && !S.pivoted[i]) {
+      const double a = fabs(Mi[k + 1]);
+      if (a > best) {  // rows visited in ascending order: the first maximum wins ties
+        best = a;
+        bi = i;
+      }
+    }
+  }
+  if (!next) return;
+  if (threadIdx.x == 0) {
+    S.pv[blockIdx.x] = best;
+    S.pi[blockIdx.x] = bi;
+    __threadfence();
+    s_last = atomicAdd(S.count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  gj_pick_and_stage(n, k + 1, M, S, gridDim.x);
+  if (threadIdx.x == 0) *S.count = 0u;
+}
+
+// A^{-1}[k][:] = R[prow_idx[k]][:] (implicit pivoting), symmetrised
+__global__ void k_gj_extract_perm(int n, const double* __restrict__ M, const int* __restrict__ prow_idx,
+                                  double* __restrict__ G) {
+  const int64_t w = 2 * (int64_t)n;
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * TB) {
+    const int64_t i = t / n, j = t % n;
+    G[t] = 0.5 * (M[(int64_t)prow_idx[i] * w + n + j] + M[(int64_t)prow_idx[j] * w + n + i]);
+  }
+}
+
 __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __restrict__ G) {
   const int64_t w = 2 * (int64_t)n;
   for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * TB) {
@@ -2142,17 +2296,43 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       AJ_LAUNCHED();
       // one (pivot, eliminate) launch pair per column; the elimination touches only the
       // columns j > k that are still read (left part) or returned (right part)
-      const int gy = std::min(nc, 1024);
-      for (int k = 0; k < nc; ++k) {
-        k_gj_pivot<<<1, TB, 0, st>>>(nc, k, M, fcol, sing);
+      if (getenv("AJ_GJ_STEPS")) {  // testing: the two-launch-per-column reference path
+        const int gy = std::min(nc, 1024);
+        for (int k = 0; k < nc; ++k) {
+          k_gj_pivot<<<1, TB, 0, st>>>(nc, k, M, fcol, sing);
+          AJ_LAUNCHED();
+          const int gx = std::max(1, std::min(ceil_div(2 * nc - k - 1, TB), 8));
+          k_gj_elim<<<dim3(gx, gy), TB, 0, st>>>(nc, k, M, fcol);
+          AJ_LAUNCHED();
+        }
+        AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
+        k_gj_extract<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, K->G);
         AJ_LAUNCHED();
-        const int gx = std::max(1, std::min(ceil_div(2 * nc - k - 1, TB), 8));
-        k_gj_elim<<<dim3(gx, gy), TB, 0, st>>>(nc, k, M, fcol);
+      } else {
+        const int gs = std::min(nc, num_sms() * (getenv("AJ_GJ_CTAS") ? atoi(getenv("AJ_GJ_CTAS")) : 4));
+        GjState S;
+        S.prow_idx = dalloc<int>(nc, st);
+        S.pivoted = dalloc<int8_t>(nc, st);
+        S.prow = dalloc<double>(4 * (int64_t)nc, st);
+        S.pv = dalloc<double>(gs, st);
+        S.pi = dalloc<int>(gs, st);
+        S.count = dalloc<unsigned int>(1, st);
+        S.singular = sing;
+        AJ_CUDA(cudaMemsetAsync(S.pivoted, 0, nc, st));
+        AJ_CUDA(cudaMemsetAsync(S.count, 0, sizeof(unsigned int), st));
+        k_gj_first<<<1, TB, 0, st>>>(nc, M, S);
         AJ_LAUNCHED();
+        for (int k = 0; k < nc; ++k) {
+          k_gj_step<<<gs, TB, 0, st>>>(nc, k, M, S);
+          AJ_LAUNCHED();
+        }
+        AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
+        k_gj_extract_perm<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, S.prow_idx,
+                                                                                               K->G);
+        AJ_LAUNCHED();
+        for (void* q : {(void*)S.prow_idx, (void*)S.pivoted, (void*)S.prow, (void*)S.pv, (void*)S.pi, (void*)S.count})
+          dfree(q, st);
       }
-      AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
-      k_gj_extract<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, K->G);
-      AJ_LAUNCHED();
       dfree(M, st);
       dfree(fcol, st);
       dfree(sing, st);

@@ -177,6 +177,26 @@ def test_precond_backward_group_sizes_agree(gpu_lib, monkeypatch):
         assert torch.linalg.norm(z - zs[None]) <= 1e-13 * torch.linalg.norm(zs[None]), gb
 
 
+def test_coarse_inverse_paths_agree(gpu_lib, monkeypatch):
+    # one-launch-per-column Gauss-Jordan with implicit pivoting (default) == the
+    # swap-based two-launch path, bit for bit (same pivots, same per-element arithmetic)
+    import torch
+    L = 14
+    eps_g = gpu_eps(gpu_lib, L, 16.5, 3)
+    r = T(rand_vec(L ** 3, 8))
+    zs = []
+    for steps in (False, True):
+        if steps:
+            monkeypatch.setenv("AJ_GJ_STEPS", "1")
+        K = gpu_lib.Precond(eps_g, L, -1.0, 0.0, gpu_lib.default_precond_params(n_coarse_max=600))
+        assert K.info()["coarse_n"] > 100
+        z = torch.empty_like(r)
+        K.apply(z, r)
+        K.free()
+        zs.append(z)
+    assert torch.equal(zs[0], zs[1])
+
+
 def test_precond_exactness_limit_gpu(gpu_lib):
     # no dropping, no kappa bound, true independent sets -> K^{-1} = (A - sigma I)^{-1}
     import torch

@@ -285,13 +285,18 @@ def big_roofline(binding, L, peak, Lp):
     return out
 
 
+def replica_seed(cfg, rank):
+    """N>1 (DESIGN.md sect. 6): one independent disorder realisation per rank."""
+    return cfg["seed"] + rank
+
+
 def run_ours(args, cfg, ws, rank, local):
     import numpy as np
     import torch
 
     from paper_math_0508111_b200 import binding
     k, L = cfg["k"], cfg["L"]
-    seed = cfg["seed"] + rank
+    seed = replica_seed(cfg, rank)
     n = L ** 3
     dev = torch.device("cuda", local if ws > 1 else 0)
     eps = torch.empty(n, dtype=torch.float64, device=dev)

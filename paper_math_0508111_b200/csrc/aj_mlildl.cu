@@ -979,10 +979,13 @@ __global__ void __launch_bounds__(SW * 32, 2)
 // neighbour c' appears at most once per block, so threads never share a slot
 // inside a block.  Rows that still do not fit are queued to ovf_list.
 constexpr int CT = 256;
-constexpr int HTC = 16384;
+constexpr int HTC_A = 8192;    // tier 2a: 96 KB of shared memory, two CTAs (rows) per SM
+constexpr int HTC_B = 16384;   // tier 2b: 192 KB, one CTA per SM
 constexpr int BMAXC = 2048;
-constexpr size_t kSchurCtaSmem = (size_t)HTC * (sizeof(int32_t) + sizeof(double));
-constexpr size_t schur_cta_scratch_words() { return (size_t)HTC * 4 + (size_t)BMAXC * (sizeof(BlkEnt) / 4 + 1); }
+template <int HT2>
+constexpr size_t schur_cta_smem() { return (size_t)HT2 * (sizeof(int32_t) + sizeof(double)); }
+template <int HT2>
+constexpr size_t schur_cta_scratch_words() { return (size_t)HT2 * 4 + (size_t)BMAXC * (sizeof(BlkEnt) / 4 + 1); }
 
 __device__ __forceinline__ void cta_bitonic_sort_kv(int32_t* a, double* v, int P) {
   for (int k = 2; k <= P; k <<= 1) {
@@ -1006,7 +1009,8 @@ __device__ __forceinline__ void cta_bitonic_sort_kv(int32_t* a, double* v, int P
   }
 }
 
-__global__ void __launch_bounds__(CT, 1)
+template <int HTC>
+__global__ void __launch_bounds__(CT, HTC <= 8192 ? 2 : 1)
     k_schur_cta(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
                 const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
                 const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
@@ -1024,7 +1028,7 @@ __global__ void __launch_bounds__(CT, 1)
   double* vals = reinterpret_cast<double*>(smem_raw);
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)HTC * sizeof(double));
   const int tid = threadIdx.x, lane = tid & 31;
-  int32_t* wscr = scratch_all + (size_t)blockIdx.x * schur_cta_scratch_words();
+  int32_t* wscr = scratch_all + (size_t)blockIdx.x * schur_cta_scratch_words<HTC>();
   int32_t* list = wscr;                                          // HTC int32 (slot list)
   double* kvals = reinterpret_cast<double*>(wscr + HTC);         // HTC doubles
   int32_t* keys2 = wscr + 3 * HTC;                               // HTC int32
@@ -2040,10 +2044,14 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     static bool attr_set = false;
     if (!attr_set) {
       AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
-      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurCtaSmem));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)schur_cta_smem<HTC_A>()));
+      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)schur_cta_smem<HTC_B>()));
       attr_set = true;
     }
     int32_t* ovf2_list = nullptr;
+    int32_t* ovf3_list = nullptr;
     int32_t* scrc = nullptr;
     int64_t cap = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
     int64_t lcap = std::max<int64_t>((int64_t)nC * 64, 1024);
@@ -2074,23 +2082,40 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
         k_iota<<<g, TB, 0, st>>>(nC, ovf_list);
         AJ_LAUNCHED();
       }
+      // AJ_SCHUR_TIER (testing): 2 = start at tier 2a, 4 = at tier 2b, 3 = at tier 3
       int nov2 = 0;
-      if (nov > 0 && first_tier >= 3) {
+      if (nov > 0 && first_tier == 3) {
         nov2 = nov;
         if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
         k_iota<<<g, TB, 0, st>>>(nC, ovf2_list);
         AJ_LAUNCHED();
       } else if (nov > 0) {
-        // tier 2: one CTA per row, 16384-entry shared-memory table
-        if (!scrc) scrc = dalloc<int32_t>((size_t)gsg2 * schur_cta_scratch_words(), st);
+        if (!scrc) scrc = dalloc<int32_t>((size_t)2 * gsg2 * schur_cta_scratch_words<HTC_B>(), st);
         if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
-        AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
-        k_schur_cta<<<std::min(nov, gsg2), CT, kSchurCtaSmem, st>>>(
-            nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
-            P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
-            ltmp_val, lcap, cursor + 1, ovf2_list, ovf + 2);
-        AJ_LAUNCHED();
-        nov2 = read_scalar(ovf + 2, st);
+        if (!ovf3_list) ovf3_list = dalloc<int32_t>(std::max(nov, 1), st);
+        const int32_t* in_list = ovf_list;
+        int nin = nov;
+        if (first_tier != 4) {
+          // tier 2a: one CTA per row, 8192-entry shared-memory table, two rows per SM
+          AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
+          k_schur_cta<HTC_A><<<std::min(nov, 2 * gsg2), CT, schur_cta_smem<HTC_A>(), st>>>(
+              nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
+              P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
+              ltmp_val, lcap, cursor + 1, ovf3_list, ovf + 2);
+          AJ_LAUNCHED();
+          nin = read_scalar(ovf + 2, st);
+          in_list = ovf3_list;
+        }
+        if (nin > 0) {
+          // tier 2b: one CTA per row, 16384-entry shared-memory table
+          AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
+          k_schur_cta<HTC_B><<<std::min(nin, gsg2), CT, schur_cta_smem<HTC_B>(), st>>>(
+              nin, in_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
+              P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
+              ltmp_val, lcap, cursor + 1, ovf2_list, ovf + 2);
+          AJ_LAUNCHED();
+          nov2 = read_scalar(ovf + 2, st);
+        }
       }
       if (nov2 > 0) {
         // tier 3: one warp per row, 32768-entry tables in global memory
@@ -2167,6 +2192,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     if (scrg) dfree(scrg, st);
     if (scrc) dfree(scrc, st);
     if (ovf2_list) dfree(ovf2_list, st);
+    if (ovf3_list) dfree(ovf3_list, st);
     for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val, (void*)cursor, (void*)row_off,
                     (void*)lrow_off, (void*)lrow_cnt})
       dfree(q, st);

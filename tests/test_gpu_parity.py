@@ -130,9 +130,9 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
     K.free()
 
 
-@pytest.mark.parametrize("tier", [2, 3])
+@pytest.mark.parametrize("tier", [2, 3, 4])
 def test_precond_schur_tiers_agree(gpu_lib, monkeypatch, tier):
-    # the CTA-per-row (tier 2) and global-table (tier 3) Schur variants compute the
+    # the CTA-per-row (tiers 2a = 2, 2b = 4) and global-table (tier 3) Schur variants compute the
     # same level structure and the same factor, bit for bit, as the warp variant
     import torch
     L = 16

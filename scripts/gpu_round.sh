@@ -1,6 +1,5 @@
-# full GPU evidence pass: tests, smoke, bench, ncu launch list of the bench step
+# full GPU evidence pass: tests, smoke, bench (default config), bench JSON into gpurun_out
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 3000 gpurun_out/bench.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --big-L 0 --precond-L 0 > gpurun_out/bench_ncu.log 2>&1; echo "ncu rc=$?"
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; head -c 400 gpurun_out/bench.json

@@ -214,9 +214,11 @@ def test_precond_exactness_limit_gpu(gpu_lib):
     K.free()
 
 
-def test_precond_symmetric_gpu(gpu_lib):
+@pytest.mark.parametrize("L", [20, 100])
+def test_precond_symmetric_gpu(gpu_lib, L):
+    # K^{-1} is symmetric at any size (L=100: production parameters, 66 levels, the
+    # Schur tiers 2a/2b in use) -- a property the oracle cannot check at that size
     import torch
-    L = 20
     eps = gpu_eps(gpu_lib, L, 16.5, 9)
     K = gpu_lib.Precond(eps, L, -1.0, 0.0)
     r1, r2 = T(rand_vec(L ** 3, 1)), T(rand_vec(L ** 3, 2))
@@ -224,7 +226,8 @@ def test_precond_symmetric_gpu(gpu_lib):
     K.apply(z1, r1)
     K.apply(z2, r2)
     a, b = float(r2 @ z1), float(r1 @ z2)
-    assert abs(a - b) <= 1e-10 * max(abs(a), abs(b))
+    scale = float(torch.linalg.norm(r1)) * max(float(torch.linalg.norm(z1)), float(torch.linalg.norm(z2)))
+    assert abs(a - b) <= 1e-10 * max(abs(a), abs(b)) or abs(a - b) <= 1e-13 * scale
     K.free()
 
 

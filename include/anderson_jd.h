@@ -64,6 +64,32 @@ AJ_API int spmv(double* d_y, const double* d_x, const double* d_eps, int32_t L, 
          double sigma, void* stream);
 
 /* ------------------------------------------------------------------------- *
+ * z-slab shard of the lattice (north star: "the lattice shards naturally into
+ * z-slabs ... with one-plane halo exchange"; DESIGN.md sect. 6, row (e)).
+ *
+ * anderson_build_slab -- eps of the planes z0 <= k < z0 + nz (sites
+ * s = z0 L^2 ... (z0 + nz) L^2 - 1 of anderson_build, same generator, so the
+ * shard equals the slice of the full lattice bit for bit).
+ * d_eps: device, nz L^2 doubles, written.  Errors: AJ_ERR_ARG unless
+ * L >= 3, z0 >= 0, nz >= 1, z0 + nz <= L, W >= 0.
+ * ------------------------------------------------------------------------- */
+AJ_API int anderson_build_slab(double* d_eps, int32_t L, int32_t z0, int32_t nz, double W, uint64_t seed,
+                               void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * spmv_slab -- y = (A - sigma I) x on a slab of nz planes (same operator as
+ * spmv), periodic in x and y.  d_x_ext: device,
+ * (nz + 2) L^2 doubles: plane 0 = the plane below the slab (global z0 - 1,
+ * periodic), planes 1..nz = the slab, plane nz + 1 = the plane above; the
+ * caller fills the two halo planes (binding: slab.halo_exchange over
+ * torch.distributed).  d_eps: nz L^2 (anderson_build_slab); d_y: nz L^2,
+ * must not alias d_x_ext.  Errors: AJ_ERR_ARG on null pointers, L < 3,
+ * nz < 1 or nz > L.
+ * ------------------------------------------------------------------------- */
+AJ_API int spmv_slab(double* d_y, const double* d_x_ext, const double* d_eps, int32_t L, int32_t nz,
+                     double hop, double sigma, void* stream);
+
+/* ------------------------------------------------------------------------- *
  * Symmetric multilevel incomplete LDL^T preconditioner K ~ A - sigma I
  * (sect. 7, l.790-973), independent-set levels (DESIGN.md sect. 3.3):
  * level 0 = red sites of the bipartite lattice, deeper levels = maximal

@@ -14,7 +14,8 @@ LIB_PATH = os.path.join(HERE, "libanderson_jd.so")
 AJ_OK, AJ_ERR_ARG, AJ_ERR_CUDA, AJ_ERR_BREAKDOWN, AJ_ERR_NOCONV, AJ_ERR_CAPACITY = range(6)
 
 # every symbol include/anderson_jd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["aj_last_error", "aj_version", "anderson_build", "spmv", "aj_precond_default_params",
+EXPORTS = ["aj_last_error", "aj_version", "anderson_build", "spmv", "anderson_build_slab", "spmv_slab",
+           "aj_precond_default_params",
            "precond_setup", "precond_apply", "precond_info", "precond_free", "sqmr_solve", "multi_dot",
            "ortho_cgs2", "aj_jd_default_params", "jd_solve", "jd_solve_host", "aj_launch_count",
            "aj_prof_enable", "aj_prof_get"]
@@ -93,6 +94,8 @@ def lib():
             "aj_last_error": ([], ctypes.c_char_p), "aj_version": ([], ctypes.c_char_p),
             "anderson_build": ([vp, i32, d, u64, vp], ctypes.c_int),
             "spmv": ([vp, vp, vp, i32, d, d, vp], ctypes.c_int),
+            "anderson_build_slab": ([vp, i32, i32, i32, d, u64, vp], ctypes.c_int),
+            "spmv_slab": ([vp, vp, vp, i32, i32, d, d, vp], ctypes.c_int),
             "aj_precond_default_params": ([ctypes.POINTER(PrecondParams)], None),
             "precond_setup": ([ctypes.POINTER(vp), vp, i32, d, d, ctypes.POINTER(PrecondParams), vp], ctypes.c_int),
             "precond_apply": ([vp, vp, vp, vp], ctypes.c_int),
@@ -162,6 +165,18 @@ def anderson_build(eps, L, W, seed):
 
 def spmv(y, x, eps, L, hop, sigma=0.0):
     _check(lib().spmv(_ptr(y), _ptr(x), _ptr(eps), L, hop, sigma, _stream()))
+    return y
+
+
+def anderson_build_slab(eps, L, z0, nz, W, seed):
+    """eps of planes [z0, z0 + nz) (z-slab shard), bit-identical to the full lattice's slice."""
+    _check(lib().anderson_build_slab(_ptr(eps), L, z0, nz, W, seed, _stream()))
+    return eps
+
+
+def spmv_slab(y, x_ext, eps, L, nz, hop, sigma=0.0):
+    """y = (A - sigma I) x on a slab; x_ext = [halo below | nz planes | halo above]."""
+    _check(lib().spmv_slab(_ptr(y), _ptr(x_ext), _ptr(eps), L, nz, hop, sigma, _stream()))
     return y
 
 

@@ -80,6 +80,24 @@ int spmv(double* d_y, const double* d_x, const double* d_eps, int32_t L, double 
   });
 }
 
+int anderson_build_slab(double* d_eps, int32_t L, int32_t z0, int32_t nz, double W, uint64_t seed, void* stream) {
+  if (!d_eps || L < 3 || z0 < 0 || nz < 1 || z0 + nz > L || !(W >= 0.0))
+    return fail(AJ_ERR_ARG, "anderson_build_slab: need d_eps, L >= 3, 0 <= z0, 1 <= nz, z0 + nz <= L, W >= 0");
+  return guarded("anderson_build_slab", [&] {
+    aj::launch_disorder_slab(d_eps, L, z0, nz, W, seed, S(stream));
+    return AJ_OK;
+  });
+}
+
+int spmv_slab(double* d_y, const double* d_x_ext, const double* d_eps, int32_t L, int32_t nz, double hop,
+              double sigma, void* stream) {
+  if (!d_y || !d_x_ext || !d_eps || L < 3 || nz < 1 || nz > L) return fail(AJ_ERR_ARG, "spmv_slab: bad arguments");
+  return guarded("spmv_slab", [&] {
+    aj::launch_spmv_slab(d_y, d_x_ext, d_eps, L, nz, hop, sigma, S(stream));
+    return AJ_OK;
+  });
+}
+
 void aj_precond_default_params(aj_precond_params* p) {
   if (!p) return;
   p->kappa = 5.0;

@@ -26,6 +26,10 @@ void launch_spmv(double* y, const double* x, const double* eps, int L, double ho
 void launch_spmv_dots(double* y, const double* x, const double* eps, int L, double hop, double sig,
                       const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st);
 int spmv_grid_blocks(int L);
+// z-slab shard: planes [z0, z0 + nz) of the disorder; SpMV with halo planes (x_ext: nz + 2 planes)
+void launch_disorder_slab(double* eps, int L, int z0, int nz, double W, uint64_t seed, cudaStream_t st);
+void launch_spmv_slab(double* y, const double* x_ext, const double* eps, int L, int nz, double hop, double sig,
+                      cudaStream_t st);
 
 // --- tall skinny (aj_blas.cu) ---
 // out[0..m) = V^T x   (out device, padded to a multiple of 8)

@@ -207,4 +207,62 @@ void launch_spmv_dots(double* y, const double* x, const double* eps, int L, doub
   AJ_LAUNCHED();
 }
 
+// ---- z-slab shard (DESIGN.md sect. 6, row (e)) --------------------------------
+// Disorder of planes [z0, z0 + nz): the same counter stream as k_disorder, indexed by
+// the global site, so the shards of a lattice are bit-identical to its slices.
+__global__ void k_disorder_slab(double* __restrict__ eps, int64_t s0, int64_t n, double W, uint64_t seed) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    double u = uniform01(seed, (uint64_t)(s0 + s));
+    eps[s] = (u - 0.5) * W;
+  }
+}
+
+void launch_disorder_slab(double* eps, int L, int z0, int nz, double W, uint64_t seed, cudaStream_t st) {
+  const int64_t P = (int64_t)L * L, n = P * nz;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 16));
+  k_disorder_slab<<<grid, 256, 0, st>>>(eps, P * z0, n, W, seed);
+  AJ_LAUNCHED();
+}
+
+// y = (A - sig I) x on a slab of nz planes: x_ext holds nz + 2 planes, plane 0 the
+// halo below (global plane z0 - 1), planes 1..nz the slab, plane nz + 1 the halo above;
+// periodic in x and y.  Same z-marching tile and the same summation order as k_spmv.
+__global__ void __launch_bounds__(SBX* SBY)
+    k_spmv_slab(double* __restrict__ y, const double* __restrict__ xe, const double* __restrict__ eps, int L,
+                int nz, double hop, double sig, int kchunk) {
+  const int i = blockIdx.x * SBX + threadIdx.x;
+  const int j = blockIdx.y * SBY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, nz);
+  if (i >= L || j >= L || k0 >= nz) return;
+  const int64_t P = (int64_t)L * L;
+  const int im = (i == 0) ? L - 1 : i - 1, ip = (i == L - 1) ? 0 : i + 1;
+  const int jm = (j == 0) ? L - 1 : j - 1, jp = (j == L - 1) ? 0 : j + 1;
+  const int64_t r0 = (int64_t)j * L, rm = (int64_t)jm * L, rp = (int64_t)jp * L;
+  double xm = __ldg(&xe[(int64_t)k0 * P + r0 + i]);        // global plane z0 + k0 - 1
+  double xc = __ldg(&xe[(int64_t)(k0 + 1) * P + r0 + i]);
+  for (int k = k0; k < k1; ++k) {
+    const double xp = __ldg(&xe[(int64_t)(k + 2) * P + r0 + i]);
+    const int64_t b = (int64_t)(k + 1) * P;
+    const double s = (__ldg(&xe[b + r0 + im]) + __ldg(&xe[b + r0 + ip])) +
+                     (__ldg(&xe[b + rm + i]) + __ldg(&xe[b + rp + i])) + (xm + xp);
+    const int64_t o = (int64_t)k * P + r0 + i;
+    y[o] = hop * s + (__ldg(&eps[o]) - sig) * xc;
+    xm = xc;
+    xc = xp;
+  }
+}
+
+void launch_spmv_slab(double* y, const double* x_ext, const double* eps, int L, int nz, double hop, double sig,
+                      cudaStream_t st) {
+  const int tiles = ceil_div(L, SBX) * ceil_div(L, SBY);
+  int zb = std::max(1, std::min(nz, ceil_div(num_sms() * 8, tiles)));
+  int kc = std::max(1, ceil_div(nz, zb));
+  zb = ceil_div(nz, kc);
+  ProfScope ps(PROF_SPMV, 24.0 * L * L * nz, st);
+  k_spmv_slab<<<dim3(ceil_div(L, SBX), ceil_div(L, SBY), zb), dim3(SBX, SBY), 0, st>>>(y, x_ext, eps, L, nz, hop,
+                                                                                        sig, kc);
+  AJ_LAUNCHED();
+}
+
 }  // namespace aj

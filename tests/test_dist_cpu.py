@@ -55,3 +55,57 @@ def test_bench_plumbing_world_size_2():
     assert m0 == m1 == 20.0           # max over ranks reaches every rank
     assert s1 == s0 + 1               # distinct realisations per rank
     assert not np.isclose(e0, e1)
+
+
+def _halo_worker(rank, ws, port, L, out):
+    os.environ.update(WORLD_SIZE=str(ws), RANK=str(rank), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_math_0508111_b200 import slab
+    dist.init_process_group("gloo")
+    z0, nz = slab.slab_bounds(L, rank, ws)
+    P = L * L
+    full = torch.arange(L * P, dtype=torch.float64)        # x_s = s: every plane is identifiable
+    x_ext = torch.full(((nz + 2) * P,), -1.0, dtype=torch.float64)
+    x_ext[P:(nz + 1) * P] = full[z0 * P:(z0 + nz) * P]
+    slab.halo_exchange(x_ext, L, nz)
+    lo_ok = torch.equal(x_ext[:P], full[((z0 - 1) % L) * P:((z0 - 1) % L + 1) * P])
+    hi_ok = torch.equal(x_ext[(nz + 1) * P:], full[((z0 + nz) % L) * P:((z0 + nz) % L + 1) * P])
+    out.put((rank, z0, nz, bool(lo_ok), bool(hi_ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("ws,L", [(2, 5), (3, 7)])
+def test_slab_halo_exchange(ws, L):
+    # z-slab sharding (row (e)): uneven slab bounds cover the lattice; every rank's halo
+    # planes are its periodic neighbours' boundary planes after one exchange
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, ws, port, L, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum(nz for _, _, nz, _, _ in res) == L
+    assert [z0 for _, z0, _, _, _ in res] == sorted(z0 for _, z0, _, _, _ in res)
+    assert all(lo and hi for _, _, _, lo, hi in res)
+
+
+def test_slab_bounds_and_single_rank_halo():
+    import torch
+    sys.path.insert(0, ROOT)
+    from paper_math_0508111_b200 import slab
+    assert [slab.slab_bounds(10, r, 3) for r in range(3)] == [(0, 4), (4, 3), (7, 3)]
+    L, P = 4, 16
+    x = torch.arange(L * P, dtype=torch.float64)
+    xe = torch.cat([torch.zeros(P, dtype=torch.float64), x, torch.zeros(P, dtype=torch.float64)])
+    slab.halo_exchange(xe, L, L)                     # one rank: periodic wrap
+    assert torch.equal(xe[:P], x[(L - 1) * P:]) and torch.equal(xe[(L + 1) * P:], x[:P])

@@ -63,6 +63,50 @@ def test_spmv_parity(gpu_lib, L, hop, sigma):
     assert err <= 1e-14 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("L,world", [(12, 3), (17, 4), (64, 8)])
+def test_slab_shards_match_full_lattice(gpu_lib, L, world):
+    # row (e) building blocks in one process: each z-slab's disorder is the slice of the
+    # full lattice bit for bit, and the slab stencil with its two halo planes (taken here
+    # from the neighbours' planes, as the NCCL exchange delivers them) reproduces the
+    # full SpMV on its planes
+    import torch
+    from paper_math_0508111_b200 import slab
+    W, seed, hop, sigma = 16.5, 3, -1.0, 0.25
+    P = L * L
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    x = T(rand_vec(L ** 3, 4))
+    y = torch.empty_like(x)
+    gpu_lib.spmv(y, x, eps, L, hop, sigma)
+    for r in range(world):
+        z0, nz = slab.slab_bounds(L, r, world)
+        es = torch.empty(nz * P, dtype=torch.float64, device="cuda")
+        gpu_lib.anderson_build_slab(es, L, z0, nz, W, seed)
+        assert torch.equal(es, eps[z0 * P:(z0 + nz) * P])
+        planes = [(z0 - 1) % L] + list(range(z0, z0 + nz)) + [(z0 + nz) % L]
+        xe = torch.cat([x[k * P:(k + 1) * P] for k in planes])
+        ys = torch.empty(nz * P, dtype=torch.float64, device="cuda")
+        gpu_lib.spmv_slab(ys, xe, es, L, nz, hop, sigma)
+        ref = y[z0 * P:(z0 + nz) * P]
+        assert torch.linalg.norm(ys - ref) <= 1e-14 * torch.linalg.norm(ref)
+
+
+def test_spmv_sharded_single_rank(gpu_lib):
+    # one rank: the halo exchange wraps periodically and spmv_sharded equals spmv
+    import torch
+    from paper_math_0508111_b200 import slab
+    L = 10
+    P = L * L
+    eps = gpu_eps(gpu_lib, L, 16.5, 1)
+    x = T(rand_vec(L ** 3, 2))
+    y = torch.empty_like(x)
+    gpu_lib.spmv(y, x, eps, L, -1.0, 0.0)
+    xe = torch.zeros((L + 2) * P, dtype=torch.float64, device="cuda")
+    xe[P:(L + 1) * P] = x
+    ys = torch.empty_like(x)
+    slab.spmv_sharded(ys, xe, eps, L, L, -1.0, 0.0)
+    assert torch.linalg.norm(ys - y) <= 1e-14 * torch.linalg.norm(y)
+
+
 def test_spmv_plane_wave_gpu(gpu_lib):
     # closed form independent of the oracle: plane wave eigenfunction of the clean stencil
     import torch

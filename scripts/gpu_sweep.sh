@@ -1,8 +1,8 @@
-# tau_virtual trade-off at L=50 / 100 / 150 (setup vs JD iterations)
+# tau_drop exponent: 2e-3 (50/L)^p for p = 1.5 and 1.0 at L=150 / 200 (tau_strong, tau_virtual follow)
 mkdir -p gpurun_out
-for f in 10 20; do
-  tv50=$(python -c "print($f*0.002)"); tv100=$(python -c "print($f*0.0005)"); tv150=$(python -c "print($f*2e-3*(50/150)**2)")
-  AJ_TV=$tv50 timeout 400 python scripts/run_config.py 1 > gpurun_out/tv50_$f.log 2>&1; echo "L50 tv=${f}td"; tail -1 gpurun_out/tv50_$f.log | cut -c1-250
-  AJ_TV=$tv100 AJ_MAX_OUTER=200 timeout 400 python scripts/run_config.py 2 > gpurun_out/tv100_$f.log 2>&1; echo "L100 tv=${f}td"; tail -1 gpurun_out/tv100_$f.log | cut -c1-250
-  AJ_TV=$tv150 AJ_MAX_OUTER=200 timeout 600 python scripts/run_config.py 2 16.5 2 150 > gpurun_out/tv150_$f.log 2>&1; echo "L150 tv=${f}td"; tail -1 gpurun_out/tv150_$f.log | cut -c1-250
-done
+for L in 150 200; do for pw in 1.5 1.0; do
+td=$(python -c "print(2e-3*(50/$L)**$pw)")
+AJ_TD=$td AJ_MAX_OUTER=150 timeout 600 python scripts/run_config.py 3 16.5 3 $L > gpurun_out/sw.log 2>&1; echo "L=$L p=$pw td=$td $(tail -1 gpurun_out/sw.log | python -c 'import sys,json
+try:
+  d=json.loads(sys.stdin.read()); print(round(d["wall_s"],2), round(d["setup_ms"]), round(d["solve_ms"]), d["outer"], d["inner"], d["levels"], round(d["nnzL_per_site"],1))
+except Exception as e: print("fail")')"; done; done

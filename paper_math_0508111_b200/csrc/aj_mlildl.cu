@@ -1579,14 +1579,17 @@ constexpr int PREF = 8;  // factor entries per lane prefetched before the depend
 template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
     k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
-                const double* __restrict__ r, const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol,
-                const TV* __restrict__ Lval, double* __restrict__ rn) {
+                const double* __restrict__ r, const double* __restrict__ gsrc, const int64_t* __restrict__ Lptr,
+                const int32_t* __restrict__ Lcol, const TV* __restrict__ Lval, double* __restrict__ rn,
+                double* __restrict__ rFn, const int32_t* __restrict__ fmapn) {
+  // gsrc: the vector Lcol indexes -- r itself (level 0) or its compact pivot part rF
+  // (levels >= 1); rFn/fmapn: the next level's compact pivot part is written too
   pdl_launch_dependents();
   const int gid = blockIdx.x * TB + threadIdx.x;
   const int cp = gid / G, lane = gid % G;
   const bool act = cp < nC;
   int64_t e0 = 0, e1 = 0;
-  int c = 0;
+  int c = 0, fn = -1;
   double Dc = 0.0;
   int32_t pc[PREF];
   double pv[PREF];
@@ -1595,6 +1598,7 @@ __global__ void __launch_bounds__(TB)
     e1 = Lptr[cp + 1];
     c = cidx[cp];
     Dc = D[c];
+    if (rFn && lane == 0) fn = fmapn[cp];
 #pragma unroll
     for (int q = 0; q < PREF; ++q) {
       const int64_t e = e0 + (int64_t)q * G;
@@ -1607,12 +1611,16 @@ __global__ void __launch_bounds__(TB)
   if (act) {
 #pragma unroll
     for (int q = 0; q < PREF; ++q)
-      if (pc[q] >= 0) acc += pv[q] * __ldg(&r[pc[q]]);
-    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)Lval[e] * __ldg(&r[Lcol[e]]);
+      if (pc[q] >= 0) acc += pv[q] * __ldg(&gsrc[pc[q]]);
+    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)Lval[e] * __ldg(&gsrc[Lcol[e]]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (act && lane == 0) rn[cp] = Dc * r[c] - acc;
+  if (act && lane == 0) {
+    const double v = Dc * r[c] - acc;
+    rn[cp] = v;
+    if (fn >= 0) rFn[fn] = v;
+  }
 }
 
 // backward substitution: blocks [0, bF) take the pivot (F) rows with G lanes
@@ -1728,13 +1736,14 @@ static void launch_pdl(K kernel, int grid, cudaStream_t st, Args... args) {
 }
 
 template <int G>
-static void fwd_g(const Level& v, const double* r, double* rn, int grid, cudaStream_t st) {
+static void fwd_g(const Level& v, const double* r, const double* gsrc, double* rn, double* rFn,
+                  const int32_t* fmapn, int grid, cudaStream_t st) {
   if (v.f32)
-    launch_pdl(k_apply_fwd<G, float>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r,
-               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const float*)v.Lval, rn);
+    launch_pdl(k_apply_fwd<G, float>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc,
+               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const float*)v.Lval, rn, rFn, fmapn);
   else
-    launch_pdl(k_apply_fwd<G, double>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r,
-               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const double*)v.Lval, rn);
+    launch_pdl(k_apply_fwd<G, double>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc,
+               (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const double*)v.Lval, rn, rFn, fmapn);
 }
 template <int G>
 static void bwd_g(const Level& v, const double* r, const double* zn, double* z, int bF, int grid, cudaStream_t st) {
@@ -1750,16 +1759,21 @@ static void bwd_g(const Level& v, const double* r, const double* zn, double* z, 
                (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval);
 }
 
-static void launch_fwd(const Level& v, const double* r, double* rn, cudaStream_t st) {
+// forward step of level v: r -> rn (the next level's input), and, if `nxt` is a sparse
+// level, its compact pivot part nxt->rF
+static void launch_fwd(const Level& v, const double* r, double* rn, const Level* nxt, cudaStream_t st) {
   if (v.nC == 0) return;
   const int grid = std::max(1, ceil_div((int64_t)v.nC * v.gf, TB));
+  const double* gsrc = v.rF ? v.rF : r;  // levels >= 1 index their compact pivot part
+  double* rFn = nxt ? nxt->rF : nullptr;
+  const int32_t* fmapn = nxt ? nxt->fmap : nullptr;
   switch (v.gf) {
-    case 1: fwd_g<1>(v, r, rn, grid, st); break;
-    case 2: fwd_g<2>(v, r, rn, grid, st); break;
-    case 4: fwd_g<4>(v, r, rn, grid, st); break;
-    case 8: fwd_g<8>(v, r, rn, grid, st); break;
-    case 16: fwd_g<16>(v, r, rn, grid, st); break;
-    default: fwd_g<32>(v, r, rn, grid, st); break;
+    case 1: fwd_g<1>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
+    case 2: fwd_g<2>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
+    case 4: fwd_g<4>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
+    case 8: fwd_g<8>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
+    case 16: fwd_g<16>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
+    default: fwd_g<32>(v, r, gsrc, rn, rFn, fmapn, grid, st); break;
   }
 }
 static void launch_bwd(const Level& v, const double* r, const double* zn, double* z, cudaStream_t st) {
@@ -1797,14 +1811,15 @@ template <typename TV>
 __global__ void k_l_gather(int nC, const int64_t* __restrict__ Lptr, const int64_t* __restrict__ row_off,
                            const int32_t* __restrict__ tcol, const double* __restrict__ tval,
                            const double* __restrict__ D, int32_t* __restrict__ Lcol, TV* __restrict__ Lval,
-                           uint64_t* __restrict__ tkey, double* __restrict__ traw, const int32_t* __restrict__ fmap) {
+                           uint64_t* __restrict__ tkey, double* __restrict__ traw, const int32_t* __restrict__ fmap,
+                           int compact) {
   const int lane = threadIdx.x & 31;
   for (int cp = (blockIdx.x * TB + threadIdx.x) >> 5; cp < nC; cp += (gridDim.x * TB) >> 5) {
     const int64_t d0 = Lptr[cp], cnt = Lptr[cp + 1] - d0, s0 = row_off[cp];
     for (int64_t t = lane; t < cnt; t += 32) {
       const int32_t f = tcol[s0 + t];
       const double l = tval[s0 + t];
-      Lcol[d0 + t] = f;
+      Lcol[d0 + t] = compact ? fmap[f] : f;
       Lval[d0 + t] = (TV)(l * D[f]);
       tkey[d0 + t] = ((uint64_t)(uint32_t)fmap[f] << 32) | (uint64_t)(uint32_t)cp;  // transpose key
       traw[d0 + t] = l;
@@ -1865,7 +1880,7 @@ void Csr::release(cudaStream_t st) {
 void Level::release(cudaStream_t st) {
   for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)fidx, (void*)fmap, (void*)partner, (void*)b11, (void*)b12,
                   (void*)Lptr, (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)Vptr,
-                  (void*)Vcol, (void*)Vval, (void*)r, (void*)z})
+                  (void*)Vcol, (void*)Vval, (void*)r, (void*)z, (void*)rF})
     dfree(p, st);
 }
 
@@ -2161,10 +2176,10 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     double* traw2 = dalloc<double>(nL, st);
     if (lv.f32)
       k_l_gather<float><<<gg, TB, 0, st>>>(nC, lv.Lptr, lrow_off, ltmp_col, ltmp_val, D, lv.Lcol, (float*)lv.Lval,
-                                            tkey, traw, lv.fmap);
+                                            tkey, traw, lv.fmap, latticeL == 0 ? 1 : 0);
     else
       k_l_gather<double><<<gg, TB, 0, st>>>(nC, lv.Lptr, lrow_off, ltmp_col, ltmp_val, D, lv.Lcol, (double*)lv.Lval,
-                                             tkey, traw, lv.fmap);
+                                             tkey, traw, lv.fmap, latticeL == 0 ? 1 : 0);
     AJ_LAUNCHED();
     {
       size_t tmpb = 0;
@@ -2292,6 +2307,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       if (lev > 0) {
         lv.r = dalloc<double>(lv.n, st);
         lv.z = dalloc<double>(lv.n, st);
+        lv.rF = dalloc<double>(std::max(lv.nF, 1), st);
       }
       lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0, lv.nnzL);
       // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
@@ -2536,7 +2552,7 @@ static void precond_inner(const Precond* K, cudaStream_t st) {
   const int nl = (int)K->lv.size();
   for (int l = 1; l < nl; ++l) {
     const Level& v = K->lv[l];
-    launch_fwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].r : K->rc, st);
+    launch_fwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].r : K->rc, (l + 1 < nl) ? &K->lv[l + 1] : nullptr, st);
   }
   if (K->nc > 0) {
     const double* rin = (nl >= 1) ? K->rc : nullptr;
@@ -2562,6 +2578,7 @@ static void prepare_tail(Precond* K, cudaStream_t st) {
   for (const auto& v : K->lv)
     if (v.nnzV > 0) return;      // ... and has no virtual couplings
   if (K->lv.size() < 2) return;
+  return;  // levels >= 1 gather through their compact pivot part rF, which the cooperative path does not do
   std::vector<LevelDesc> h(K->lv.size());
   for (size_t l = 0; l < K->lv.size(); ++l) {
     const Level& v = K->lv[l];
@@ -2608,7 +2625,7 @@ void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st) 
     return;
   }
   const Level& v0 = K->lv[0];
-  launch_fwd(v0, r, (nl > 1) ? K->lv[1].r : K->rc, st);
+  launch_fwd(v0, r, (nl > 1) ? K->lv[1].r : K->rc, (nl > 1) ? &K->lv[1] : nullptr, st);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   AJ_CUDA(cudaStreamIsCapturing(st, &cs));
   if (K->tail_grid > 0) {
@@ -2630,6 +2647,7 @@ int64_t precond_bytes_per_apply(const Precond* K) {
     b += (v.nnzL + v.nnzLT) * (v.f32 ? 8 : 12) + v.nnzV * 12;
     b += (int64_t)v.n * (8 /*D*/ + 8 /*r*/ + 8 /*z*/ + 4 /*cmap*/ + 8 * 2 /*b11,b12 for F*/ + 4 /*partner*/);
     b += (int64_t)v.nC * (4 + 8 + 8 + 8);  // cidx, D_c r_c, rn write, L ptr
+    if (v.rF) b += (int64_t)v.nF * (8 + 4);  // compact pivot part written by the previous step (+ fmap)
   }
   b += (int64_t)K->nc * K->nc * 8;
   return b;

@@ -27,7 +27,7 @@ struct Level {
   double* b11 = nullptr;        // n   B^{-1}[f,f]   (F nodes)
   double* b12 = nullptr;        // n   B^{-1}[f,g]   (F nodes of a pair)
   int64_t* Lptr = nullptr;      // nC+1
-  int32_t* Lcol = nullptr;      // level index of F node
+  int32_t* Lcol = nullptr;      // F node: level index (level 0), pivot index f' (levels >= 1, gathers rF)
   void* Lval = nullptr;         // L_cf * D_f  (float if f32, else double)
   int64_t* LTptr = nullptr;     // nF+1, rows in F order
   int32_t* LTcol = nullptr;     // coarse index
@@ -38,6 +38,7 @@ struct Level {
   double* Vval = nullptr;       // b'_uv
   int64_t nnzV = 0;
   int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
+  double* rF = nullptr;         // nF: r on the pivots, compact (levels >= 1; written by the previous forward step)
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;
   void release(cudaStream_t st);

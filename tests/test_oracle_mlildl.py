@@ -195,3 +195,35 @@ def test_compensation_improves_preconditioner():
         assert res <= 1e-8
         its[comp] = it
     assert its[True] < its[False]
+
+
+def test_compensation_threshold_tau_virtual():
+    # reading R17: only couplings |a^_uv| >= tau_virtual become virtual blocks; below it
+    # the coupling is dropped as without compensation (same 3x3 case as above)
+    a, b, e = 0.5, 0.6, 0.01
+    A = sp.csr_matrix(np.array([[1.0, e, a], [e, 1.0, b], [a, b, 1.0]]))
+    above = mlildl.factor_level(A, kappa=5.0, tau_drop=0.0, tau_strong=0.02, tau_virtual=0.005)
+    below = mlildl.factor_level(A, kappa=5.0, tau_drop=0.0, tau_strong=0.02, tau_virtual=0.02)
+    assert above.nvirtual == 1 and below.nvirtual == 0
+    assert np.isclose(above.S.toarray()[0, 0], 1.0 - (a * a + b * b - 2 * a * b * e), rtol=0, atol=1e-15)
+    assert np.isclose(below.S.toarray()[0, 0], 1.0 - (a * a + b * b), rtol=0, atol=1e-15)
+
+
+def test_compensation_adds_no_schur_fill():
+    # reading R17: the virtual terms update only the pattern of A_CC and the real blocks.
+    # Chain c0 - u - v - c1 (u = 0, v = 1 win the independent set on index ties; u - v is
+    # weak): the compensated S has no (c0, c1) entry -- it would be fill -- while L carries
+    # the first-order coupling l_{c0 v} = a_{c0 u} b'_{uv}, b'_{uv} = -(a_uv B_uu B_vv)
+    e = 0.01
+    A = np.eye(4)
+    A[0, 2] = A[2, 0] = 0.5      # u - c0
+    A[0, 1] = A[1, 0] = e        # u - v (weak)
+    A[1, 3] = A[3, 1] = 0.6      # v - c1
+    Lv = mlildl.factor_level(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.02, tau_virtual=0.0)
+    assert sorted(Lv.F) == [0, 1] and Lv.nvirtual == 1
+    S = Lv.S.toarray()
+    assert S[0, 1] == 0.0 and S[1, 0] == 0.0
+    Ld = Lv.L.toarray()
+    assert np.isclose(Ld[0, 0], 0.5, rtol=0, atol=1e-15)
+    assert np.isclose(Ld[0, 1], 0.5 * -(e * (1.0 * 1.0)), rtol=0, atol=1e-15)
+    assert np.isclose(Ld[1, 0], 0.6 * -(e * (1.0 * 1.0)), rtol=0, atol=1e-15)

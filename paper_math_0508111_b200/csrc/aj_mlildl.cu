@@ -1632,7 +1632,7 @@ __global__ void __launch_bounds__(TB)
                 const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ LTptr,
                 const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval, const double* __restrict__ zn,
                 double* __restrict__ z, const int64_t* __restrict__ Vptr, const int32_t* __restrict__ Vcol,
-                const double* __restrict__ Vval) {
+                const double* __restrict__ Vval, const double* __restrict__ rF) {
   pdl_launch_dependents();
   if ((int)blockIdx.x >= bF) {
     const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
@@ -1702,7 +1702,7 @@ __global__ void __launch_bounds__(TB)
     }
   }
   if (act && lane == 0) {
-    double y = B1 * (Di * r[i]);
+    double y = B1 * (Di * (rF ? rF[fp] : r[i]));  // rF: the level's input on its pivots, contiguous
     if (p >= 0) y += B2 * (Dp * r[p]);
     z[i] = Di * (y - acc);
   }
@@ -1751,12 +1751,12 @@ static void bwd_g(const Level& v, const double* r, const double* zn, double* z, 
     launch_pdl(k_apply_bwd<G, float>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
                (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z,
-               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval);
+               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval, (const double*)v.rF);
   else
     launch_pdl(k_apply_bwd<G, double>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
                (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z,
-               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval);
+               (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval, (const double*)v.rF);
 }
 
 // forward step of level v: r -> rn (the next level's input), and, if `nxt` is a sparse

@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--precond-L", type=int, default=150,
                     help="lattice for the preconditioner-apply roofline pass, production parameters (0=off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prof-cats", default="precond_apply,precond_setup",
+                    help="phases timed live inside the timed region (each adds two stream events per call)")
     ap.add_argument("--no-e2e", action="store_true")
     # tuning knobs (defaults = library defaults, aj_*_default_params)
     for k in ["kappa", "tau_drop", "tau_strong", "inner_tol", "switch_tol"]:
@@ -321,7 +323,7 @@ def run_ours(args, cfg, ws, rank, local):
     binding.launch_count(reset=True)
     # live timing of the heavy phases only (per-call event pairs on the launching stream);
     # the thousands of tiny JD/SQMR vector kernels are not bracketed (overhead)
-    binding.prof_enable(True, categories=["spmv", "precond_apply", "precond_setup"])
+    binding.prof_enable(True, categories=args.prof_cats.split(","))
     total_ms = 0.0
     per = []
     with ClockSampler(local if ws > 1 else 0) as clk:

@@ -11,6 +11,19 @@
 
 namespace aj {
 
+cudaStream_t capture_stream() {
+  thread_local cudaStream_t s = nullptr;
+  if (!s) AJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+double* pinned_scalars() {
+  thread_local double* p = nullptr;
+  if (!p) AJ_CUDA(cudaMallocHost(&p, 64 * sizeof(double)));
+  return p;
+}
+
+
 thread_local int64_t g_launches = 0;
 
 // ---- live profiling ------------------------------------------------------

@@ -18,6 +18,11 @@ struct RedScratch {
   RedBuf buf(double* out, int ticket = 0) const { return RedBuf{partials, tickets + ticket, out}; }
 };
 
+// --- per-host-thread resources, created once (aj_blas.cu): stream-capture stream and a
+//     small pinned host buffer; creating/freeing them per solve costs host time in the path
+cudaStream_t capture_stream();
+double* pinned_scalars();  // 64 doubles
+
 // --- lattice (aj_stencil.cu) ---
 void launch_disorder(double* eps, int L, double W, uint64_t seed, cudaStream_t st);
 void launch_spmv(double* y, const double* x, const double* eps, int L, double hop, double sig,

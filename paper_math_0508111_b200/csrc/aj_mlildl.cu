@@ -2600,8 +2600,7 @@ static void prepare_tail(Precond* K, cudaStream_t st) {
 
 static void precond_capture(Precond* K, cudaStream_t st) {
   if (K->lv.size() < 1) return;
-  cudaStream_t cs;
-  AJ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t cs = capture_stream();
   AJ_CUDA(cudaStreamSynchronize(st));
   const int64_t before = g_launches;
   AJ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -2612,7 +2611,6 @@ static void precond_capture(Precond* K, cudaStream_t st) {
   g_launches = before;
   AJ_CUDA(cudaGraphInstantiate(&K->exec, g, 0));
   AJ_CUDA(cudaGraphDestroy(g));
-  AJ_CUDA(cudaStreamDestroy(cs));
 }
 
 // z = K^{-1} r

@@ -333,8 +333,8 @@ __global__ void k_negate_proj(int64_t n, double* __restrict__ b, const double* _
 // ============================================================================
 Workspace::Workspace(int64_t n_, cudaStream_t st) : n(n_) {
   rs.init(st);
-  AJ_CUDA(cudaMallocHost(&hpin, 64 * sizeof(double)));
-  AJ_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+  hpin = pinned_scalars();       // per host thread, reused across solves
+  cap_stream = capture_stream();
   // opt-in (AJ_SQMR_GRAPH=1): capturing two graphs per correction equation costs more
   // than it saves at ~20 SQMR steps per solve (L=50 step 361 vs 337 ms)
   const char* e = getenv("AJ_SQMR_GRAPH");
@@ -345,9 +345,7 @@ Workspace::Workspace(int64_t n_, cudaStream_t st) : n(n_) {
 }
 void Workspace::release(cudaStream_t st) {
   rs.release(st);
-  if (hpin) cudaFreeHost(hpin);
-  hpin = nullptr;
-  if (cap_stream) cudaStreamDestroy(cap_stream);
+  hpin = nullptr;       // owned per host thread (pinned_scalars / capture_stream)
   cap_stream = nullptr;
   dfree(sc, st);
   dfree(small, st);

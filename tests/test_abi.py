@@ -42,6 +42,12 @@ def test_argument_errors(lib):
     assert lib.spmv(None, None, None, 10, 1.0, 0.0, None) == binding.AJ_ERR_ARG
     assert lib.precond_apply(None, None, None, None) == binding.AJ_ERR_ARG
     assert lib.precond_free(None) == binding.AJ_OK
+    # z-slab shard entry points: bounds checked before any device work
+    assert lib.anderson_build_slab(ctypes.c_void_p(16), 10, 8, 3, 1.0, 1, None) == binding.AJ_ERR_ARG
+    assert b"anderson_build_slab" in lib.aj_last_error()
+    assert lib.spmv_slab(None, None, None, 10, 2, 1.0, 0.0, None) == binding.AJ_ERR_ARG
+    assert lib.spmv_slab(ctypes.c_void_p(16), ctypes.c_void_p(32), ctypes.c_void_p(48), 10, 11, 1.0, 0.0,
+                         None) == binding.AJ_ERR_ARG
 
 
 def test_no_cpu_fallback_without_device(lib):

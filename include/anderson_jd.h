@@ -141,7 +141,10 @@ AJ_API int precond_setup(void** handle, const double* d_eps, int32_t L, double h
 /* z = K^{-1} r.  d_z, d_r: device n doubles, may not alias. Symmetric linear operator. */
 AJ_API int precond_apply(void* handle, double* d_z, const double* d_r, void* stream);
 AJ_API int precond_info(void* handle, aj_precond_info* info);
-AJ_API int precond_free(void* handle);
+/* Releases the handle.  The device is synchronised first (applies enqueued on any
+ * stream finish before the factor's memory returns to the pool), then the buffers
+ * are freed stream-ordered on `stream` and `stream` is synchronised.  NULL = no-op. */
+AJ_API int precond_free(void* handle, void* stream);
 
 /* ------------------------------------------------------------------------- *
  * sqmr_solve -- simplified QMR for

@@ -142,7 +142,7 @@ def _pair_candidates(Ah, dg, lmax1, d1, p, kappa):
             d2 += x
         lead = i if not ok1[i] else j
         if d2 < d1[lead] and lm2 <= kappa - 1:
-            pairs.append((i, j, B11, B12, B22, lm2))
+            pairs.append((i, j, B11, B12, B22, lm2, d2))
     return pairs
 
 
@@ -166,7 +166,7 @@ def _mis(nb, keyrank, edges_a, edges_b):
 
 
 def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.005, compensate=True,
-                 tau_virtual=None):
+                 tau_virtual=None, priority="quality"):
     n = A.shape[0]
     D, Ah = _scaled(A)
     dg, lmax1, d1, p = _pivot_quality(Ah)
@@ -182,7 +182,7 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
         pairs = []
     leader = np.full(n, -1, dtype=np.int64)     # block leader of each candidate node
     q = np.full(n, np.inf)                      # block quality (at the leader)
-    for (i, j, B11, B12, B22, lm2) in pairs:
+    for (i, j, B11, B12, B22, lm2, _d2) in pairs:
         partner[i], partner[j] = j, i
         b11[i], b12[i] = B11, B12
         b11[j], b12[j] = B22, B12
@@ -207,7 +207,12 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
         m = leader >= 0
         bid[m] = pos[leader[m]]
         keyrank = np.empty(nb, dtype=np.int64)
-        keyrank[np.lexsort((blk, q[blk]))] = np.arange(nb)
+        if priority == "degree":
+            rl = np.diff(Ah.indptr)
+            deg = rl[blk] + np.where(partner[blk] >= 0, rl[np.maximum(partner[blk], 0)], 0)
+            keyrank[np.lexsort((blk, q[blk], deg))] = np.arange(nb)
+        else:
+            keyrank[np.lexsort((blk, q[blk]))] = np.arange(nb)
         coo = Ah.tocoo()
         r, c, v = coo.row, coo.col, coo.data
         strong = (r != c) & (np.abs(v) >= tau_strong) & (bid[r] >= 0) & (bid[c] >= 0)
@@ -471,7 +476,7 @@ class MultilevelILDL:
 
     def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
                  n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False,
-                 compensate=True, tau_virtual=None):
+                 compensate=True, tau_virtual=None, priority="quality"):
         """factor_fp32 (reading R16): the stored factor values are rounded to
         IEEE binary32 -- forward entries as fl32(l_cf * D_f), backward entries as
         fl32(l_cf) -- and used in fp64 arithmetic, as on the GPU."""
@@ -483,7 +488,8 @@ class MultilevelILDL:
             if cur.shape[0] <= n_coarse_max:
                 break
             Lv = factor_level(cur, kappa, tau_drop, tau_strong,
-                              lattice_L if lev == 0 else None, stall_frac, compensate, tau_virtual)
+                              lattice_L if lev == 0 else None, stall_frac, compensate, tau_virtual,
+                              priority)
             if Lv is None:
                 break
             if self.factor_fp32:

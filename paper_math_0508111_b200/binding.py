@@ -100,7 +100,7 @@ def lib():
             "precond_setup": ([ctypes.POINTER(vp), vp, i32, d, d, ctypes.POINTER(PrecondParams), vp], ctypes.c_int),
             "precond_apply": ([vp, vp, vp, vp], ctypes.c_int),
             "precond_info": ([vp, ctypes.POINTER(PrecondInfo)], ctypes.c_int),
-            "precond_free": ([vp], ctypes.c_int),
+            "precond_free": ([vp, vp], ctypes.c_int),
             "sqmr_solve": ([vp, vp, vp, vp, i32, d, d, d, i32, ctypes.POINTER(i32), dp, vp], ctypes.c_int),
             "multi_dot": ([dp, vp, i32, vp, i64, vp], ctypes.c_int),
             "ortho_cgs2": ([vp, vp, i32, i64, dp, vp], ctypes.c_int),
@@ -200,7 +200,7 @@ class Precond:
 
     def free(self):
         if self.h:
-            _check(lib().precond_free(self.h))
+            _check(lib().precond_free(self.h, _stream()))
             self.h = ctypes.c_void_p()
 
     def __del__(self):

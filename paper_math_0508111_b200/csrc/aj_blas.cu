@@ -3,6 +3,7 @@
 // cores (fp64 contractions of width <= 64 sit far below the flop/byte
 // crossover, and B200's fp64 tensor path is not the bottleneck here).
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <vector>
 
@@ -11,17 +12,30 @@
 
 namespace aj {
 
+// Per-(host thread, device) resources: a stream is bound to the device that was
+// current when it was created, so the caches are keyed by the current device.
+constexpr int kMaxDev = 64;
+static int current_device() {
+  int dev = 0;
+  AJ_CUDA(cudaGetDevice(&dev));
+  AJ_REQUIRE(dev >= 0 && dev < kMaxDev, AJ_ERR_CUDA, "device ordinal out of range");
+  return dev;
+}
+
 cudaStream_t capture_stream() {
-  thread_local cudaStream_t s = nullptr;
-  if (!s) AJ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  return s;
+  thread_local cudaStream_t s[kMaxDev] = {};
+  const int dev = current_device();
+  if (!s[dev]) AJ_CUDA(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
+  return s[dev];
 }
 
 double* pinned_scalars() {
-  thread_local double* p = nullptr;
-  if (!p) AJ_CUDA(cudaMallocHost(&p, 64 * sizeof(double)));
-  return p;
+  thread_local double* p[kMaxDev] = {};
+  const int dev = current_device();
+  if (!p[dev]) AJ_CUDA(cudaMallocHost(&p[dev], 64 * sizeof(double)));
+  return p[dev];
 }
+
 
 
 thread_local int64_t g_launches = 0;
@@ -125,11 +139,12 @@ void prof_get(aj_prof* out) {
 }
 
 int num_sms() {
-  static int sms = 0;
+  static std::atomic<int> cache[kMaxDev];
+  const int dev = current_device();
+  int sms = cache[dev].load();
   if (sms == 0) {
-    int dev = 0;
-    AJ_CUDA(cudaGetDevice(&dev));
     AJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev].store(sms);
     // keep freed stream-ordered allocations mapped: the factorisation allocates and
     // frees GBs per level, and the default threshold (0) would unmap them at every
     // synchronisation and remap them at the next cudaMallocAsync

@@ -141,10 +141,14 @@ int precond_info(void* handle, aj_precond_info* info) {
   return AJ_OK;
 }
 
-int precond_free(void* handle) {
+int precond_free(void* handle, void* stream) {
   if (!handle) return AJ_OK;
   return guarded("precond_free", [&] {
-    cudaStream_t st = 0;
+    // the frees are stream-ordered on `stream` (after every apply enqueued on it);
+    // the device-wide synchronisation first also orders them after applies the
+    // caller enqueued on other streams, so no pool block is reused under a kernel
+    AJ_CUDA(cudaDeviceSynchronize());
+    cudaStream_t st = S(stream);
     aj::precond_destroy((aj::Precond*)handle, st);
     AJ_CUDA(cudaStreamSynchronize(st));
     return AJ_OK;

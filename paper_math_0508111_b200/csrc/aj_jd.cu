@@ -17,7 +17,7 @@ namespace aj {
 
 // kernels defined in aj_solver.cu
 __global__ void k_small_eig(int j, int ldm, const double* Min, double* theta, double* S);
-__global__ void k_small_inv(int m, const double* H, double* Hinv, double* sc);
+__global__ void k_small_inv(int m, const double* H, int ldh, double* Hinv, int* status);
 __global__ void k_set_mcol(double* M, int ldm, int j, const double* dots);
 __global__ void k_set_mdiag(double* M, int ldm, int cnt, const double* theta, int off);
 __global__ void k_resid(int64_t n, const double* Au, const double* u, const double* theta, double* r, RedBuf rb);
@@ -37,7 +37,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
                 const aj_precond_params& pp, const aj_jd_params& jp, double* h_lambda, double* d_X,
                 double* h_resid, aj_precond_info* pinfo, cudaStream_t st) {
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "jd_solve: L must be >= 3");
-  AJ_REQUIRE(k >= 1 && k <= 16, AJ_ERR_ARG, "jd_solve: 1 <= k <= 16");
+  AJ_REQUIRE(k >= 1 && k <= 16, AJ_ERR_ARG, "jd_solve: 1 <= k <= 16");  // m = k + 1 <= 17 (k_small_inv)
   AJ_REQUIRE(jp.jmax <= 48 && jp.jmin >= 1 && jp.jmin < jp.jmax && jp.jmax >= 2, AJ_ERR_ARG,
              "jd_solve: need 1 <= jmin < jmax <= 48");
   AJ_REQUIRE(tol > 0.0 && h_lambda, AJ_ERR_ARG, "jd_solve: tol > 0 and h_lambda required");
@@ -68,6 +68,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
   double* b = dalloc<double>(n, st);
   double* sm = dalloc<double>(16384, st);
   unsigned long long* amax = dalloc<unsigned long long>(1, st);
+  int* hstat = dalloc<int>(1, st);
   double* M = sm;            // jmax x jmax (ld jmax)
   double* S = sm + 4096;     // j x j
   double* theta = sm + 8192; // j
@@ -82,7 +83,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
   int status = AJ_OK;
   auto cleanup = [&]() {
     for (void* p : {(void*)V, (void*)AV, (void*)Vt, (void*)AVt, (void*)QT, (void*)Y, (void*)u, (void*)Au, (void*)r,
-                    (void*)z, (void*)b, (void*)sm, (void*)amax})
+                    (void*)z, (void*)b, (void*)sm, (void*)amax, (void*)hstat})
       dfree(p, st);
     ws.release(st);
     precond_destroy(K, st);
@@ -204,17 +205,17 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
       launch_copy(QT + (int64_t)nq * n, u, n, st);
       precond_run(K, Y + (int64_t)nq * n, u, st);
       for (int c = 0; c < m; ++c) launch_multi_dot(Hb + c * mpad, QT, m, n, Y + (int64_t)c * n, n, ws.rs, st);
-      // compact H (m x m, ld m) into Hinv scratch then invert
-      {
-        std::vector<double> hH((size_t)m * mpad), hc((size_t)m * m);
-        rd(hH.data(), Hb, hH.size(), st);
-        for (int c = 0; c < m; ++c)
-          for (int a = 0; a < m; ++a) hc[a + c * m] = hH[a + c * mpad];
-        AJ_CUDA(cudaMemcpyAsync(Hb, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        AJ_CUDA(cudaStreamSynchronize(st));
-      }
-      k_small_inv<<<1, 1, 0, st>>>(m, Hb, Hinv, ws.sc);
+      // Hinv = H^{-1} (H column c at Hb + c * mpad); a singular H (K^{-1} Q~ losing rank)
+      // is reported, never silently replaced by the previous outer iteration's Hinv
+      k_small_inv<<<1, 256, 0, st>>>(m, Hb, mpad, Hinv, hstat);
       AJ_LAUNCHED();
+      {
+        int hs = 0;
+        rd(&hs, hstat, 1, st);
+        AJ_REQUIRE(hs == 0, AJ_ERR_BREAKDOWN,
+                   "jd_solve: H = Q~^T K^{-1} Q~ of the projected preconditioner is singular (outer " +
+                       std::to_string(R.outer) + ")");
+      }
       const double shift = (rnorm < jp.switch_tol * normA) ? theta0 : 0.0;
       launch_multi_dot(cq, QT, m, n, r, n, ws.rs, st);
       k_negate_proj<<<sg(n), 256, 0, st>>>(n, b, r, QT, m, cq);

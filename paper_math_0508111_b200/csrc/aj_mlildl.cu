@@ -16,7 +16,6 @@
 // factor keeps L (rows = coarse nodes, cols = level index, values L_cf*D_f)
 // and L^T (rows = level nodes, cols = coarse index, values L_cf) so both
 // substitutions are pure gathers (no atomics).
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -2056,14 +2055,13 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     int32_t* ovf_list = dalloc<int32_t>(std::max(nC, 1), st);
     unsigned long long* cursor = dalloc<unsigned long long>(2, st);
     int* ovf = counters + 5;   // [5] fallback rows, [6] error
-    static bool attr_set = false;
-    if (!attr_set) {
+    {  // per level (cheap): the limit is a per-device property of the function, and the
+       // calling thread may drive a different device than on the previous setup
       AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
       AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)schur_cta_smem<HTC_A>()));
       AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)schur_cta_smem<HTC_B>()));
-      attr_set = true;
     }
     int32_t* ovf2_list = nullptr;
     int32_t* ovf3_list = nullptr;
@@ -2224,7 +2222,6 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
 }
 
 static void precond_capture(Precond* K, cudaStream_t st);
-static void prepare_tail(Precond* K, cudaStream_t st);
 
 static bool verbose_setup() {
   static int v = -1;
@@ -2287,15 +2284,7 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       Level lv;
       Csr S;
       const double t0 = verbose_setup() ? wall_ms() : 0.0;
-      aj_precond_params Pl = P;
-      {  // experimental (AJ_ROWCAP=r): raise tau_drop on levels whose matrix exceeds r entries per row
-        static const char* rc = getenv("AJ_ROWCAP");
-        if (rc && A.n > 0) {
-          const double avg = (double)A.nnz / A.n, cap = atof(rc);
-          if (avg > cap) Pl.tau_drop = P.tau_drop * (avg / cap);
-        }
-      }
-      if (!factor_level(A, lev == 0 ? L : 0, Pl, lv, S, st)) break;
+      if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
       if (verbose_setup()) {
         AJ_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
@@ -2415,13 +2404,11 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   I.tau_virtual = P.tau_virtual;
   K->bytes_per_apply = precond_bytes_per_apply(K);
   precond_capture(K, st);
-  prepare_tail(K, st);
   return K;
 }
 
 void precond_destroy(Precond* K, cudaStream_t st) {
   if (!K) return;
-  dfree(K->dlv, st);
   if (K->exec) cudaGraphExecDestroy(K->exec);
   for (auto& l : K->lv) l.release(st);
   dfree(K->G, st);
@@ -2432,122 +2419,6 @@ void precond_destroy(Precond* K, cudaStream_t st) {
 
 // levels >= 1 and the coarse solve, between internal buffers (captured once
 // into a CUDA graph at the end of precond_create)
-// ----------------------------------------------------------------------------
-// Persistent cooperative application of levels >= 1 and the coarse solve: one
-// launch, grid-wide barriers between the level phases (the phases are latency
-// bound for the small deep levels; a barrier is cheaper than a kernel boundary).
-// Vectors written inside the kernel are read with ld.global.cg (L2) so no SM
-// can see a stale L1 line; the factor itself is read-only.
-constexpr int TAIL_TB = 512;
-
-template <int G>
-__device__ __forceinline__ void tail_fwd(const LevelDesc& v, const double* __restrict__ r, double* __restrict__ rn,
-                                         int tid, int nthr) {
-  const int ngroups = nthr / G;
-  const int lane = tid % G;
-  for (int base = 0; base < v.nC; base += ngroups) {
-    const int cp = base + tid / G;
-    const bool act = cp < v.nC;
-    double acc = 0.0;
-    if (act) {
-      const int64_t e1 = v.Lptr[cp + 1];
-      for (int64_t e = v.Lptr[cp] + lane; e < e1; e += G) acc += v.Lval[e] * __ldcg(&r[v.Lcol[e]]);
-    }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (act && lane == 0) {
-      const int c = v.cidx[cp];
-      rn[cp] = v.D[c] * __ldcg(&r[c]) - acc;
-    }
-  }
-}
-
-template <int G>
-__device__ __forceinline__ void tail_bwd(const LevelDesc& v, const double* __restrict__ r, const double* __restrict__ zn,
-                                         double* __restrict__ z, int tid, int nthr) {
-  for (int cp = tid; cp < v.nC; cp += nthr) {
-    const int i = v.cidx[cp];
-    z[i] = v.D[i] * __ldcg(&zn[cp]);
-  }
-  const int ngroups = nthr / G;
-  const int lane = tid % G;
-  for (int base = 0; base < v.nF; base += ngroups) {
-    const int fp = base + tid / G;
-    const bool act = fp < v.nF;
-    double acc = 0.0;
-    if (act) {
-      const int64_t e1 = v.LTptr[fp + 1];
-      for (int64_t e = v.LTptr[fp] + lane; e < e1; e += G) acc += v.LTval[e] * __ldcg(&zn[v.LTcol[e]]);
-    }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (act && lane == 0) {
-      const int i = v.fidx[fp];
-      double y = v.b11[i] * (v.D[i] * __ldcg(&r[i]));
-      const int32_t p = v.partner[i];
-      if (p >= 0) y += v.b12[i] * (v.D[p] * __ldcg(&r[p]));
-      z[i] = v.D[i] * (y - acc);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(TAIL_TB) k_apply_tail(const LevelDesc* __restrict__ lv, int nl,
-                                                        const double* __restrict__ Gm, int nc, double* rc, double* zc) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  const int nthr = gridDim.x * TAIL_TB;
-  const int tid = blockIdx.x * TAIL_TB + threadIdx.x;
-  for (int l = 1; l < nl; ++l) {
-    const LevelDesc v = lv[l];
-    double* rn = (l + 1 < nl) ? lv[l + 1].r : rc;
-    switch (v.gf) {
-      case 1: tail_fwd<1>(v, v.r, rn, tid, nthr); break;
-      case 2: tail_fwd<2>(v, v.r, rn, tid, nthr); break;
-      case 4: tail_fwd<4>(v, v.r, rn, tid, nthr); break;
-      case 8: tail_fwd<8>(v, v.r, rn, tid, nthr); break;
-      case 16: tail_fwd<16>(v, v.r, rn, tid, nthr); break;
-      default: tail_fwd<32>(v, v.r, rn, tid, nthr); break;
-    }
-    grid.sync();
-  }
-  // coarse z_c = G r_c, one warp per row
-  {
-    const int lane = tid & 31, nw = nthr >> 5;
-    for (int i = tid >> 5; i < nc; i += nw) {
-      double acc = 0.0;
-      for (int j = lane; j < nc; j += 32) acc += Gm[(int64_t)i * nc + j] * __ldcg(&rc[j]);
-      acc = warp_sum(acc);
-      if (lane == 0) zc[i] = acc;
-    }
-  }
-  grid.sync();
-  for (int l = nl - 1; l >= 1; --l) {
-    const LevelDesc v = lv[l];
-    const double* zn = (l + 1 < nl) ? lv[l + 1].z : zc;
-    switch (v.gb) {
-      case 1: tail_bwd<1>(v, v.r, zn, v.z, tid, nthr); break;
-      case 2: tail_bwd<2>(v, v.r, zn, v.z, tid, nthr); break;
-      case 4: tail_bwd<4>(v, v.r, zn, v.z, tid, nthr); break;
-      case 8: tail_bwd<8>(v, v.r, zn, v.z, tid, nthr); break;
-      case 16: tail_bwd<16>(v, v.r, zn, v.z, tid, nthr); break;
-      default: tail_bwd<32>(v, v.r, zn, v.z, tid, nthr); break;
-    }
-    if (l > 1) grid.sync();
-  }
-}
-
-static void launch_tail(const Precond* K, cudaStream_t st) {
-  const LevelDesc* lv = K->dlv;
-  int nl = (int)K->lv.size();
-  const double* Gm = K->G;
-  int nc = K->nc;
-  double* rc = K->rc;
-  double* zc = K->zc;
-  void* args[] = {(void*)&lv, (void*)&nl, (void*)&Gm, (void*)&nc, (void*)&rc, (void*)&zc};
-  AJ_CUDA(cudaLaunchCooperativeKernel((const void*)k_apply_tail, dim3(K->tail_grid), dim3(TAIL_TB), args, 0, st));
-  AJ_LAUNCHED();
-}
-
 static void precond_inner(const Precond* K, cudaStream_t st) {
   const int nl = (int)K->lv.size();
   for (int l = 1; l < nl; ++l) {
@@ -2565,37 +2436,6 @@ static void precond_inner(const Precond* K, cudaStream_t st) {
     const Level& v = K->lv[l];
     launch_bwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].z : K->zc, v.z, st);
   }
-}
-
-static void prepare_tail(Precond* K, cudaStream_t st) {
-  K->tail_grid = 0;
-  // opt-in (AJ_TAIL=1): measured slower than the captured per-level graph on B200
-  // (grid-wide barriers cost more than graph kernel boundaries: L=50 0.61 vs
-  // 0.36 ms, L=250 17.4 vs 7.2 ms per apply)
-  const char* e = getenv("AJ_TAIL");
-  if (!(e && atoi(e) == 1)) return;
-  if (K->P.factor_fp32) return;  // the cooperative path reads fp64 factors only
-  for (const auto& v : K->lv)
-    if (v.nnzV > 0) return;      // ... and has no virtual couplings
-  if (K->lv.size() < 2) return;
-  return;  // levels >= 1 gather through their compact pivot part rF, which the cooperative path does not do
-  std::vector<LevelDesc> h(K->lv.size());
-  for (size_t l = 0; l < K->lv.size(); ++l) {
-    const Level& v = K->lv[l];
-    LevelDesc& d = h[l];
-    d.n = v.n; d.nF = v.nF; d.nC = v.nC; d.gf = v.gf; d.gb = v.gb;
-    d.cidx = v.cidx; d.fidx = v.fidx; d.partner = v.partner; d.D = v.D; d.b11 = v.b11; d.b12 = v.b12;
-    d.Lptr = v.Lptr; d.LTptr = v.LTptr; d.Lcol = v.Lcol; d.LTcol = v.LTcol;
-    d.Lval = (const double*)v.Lval; d.LTval = (const double*)v.LTval;
-    d.r = v.r; d.z = v.z;
-  }
-  K->dlv = dalloc<LevelDesc>(h.size(), st);
-  AJ_CUDA(cudaMemcpyAsync(K->dlv, h.data(), h.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, st));
-  AJ_CUDA(cudaStreamSynchronize(st));
-  int per_sm = 0;
-  AJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_tail, TAIL_TB, 0));
-  if (per_sm < 1) return;
-  K->tail_grid = num_sms() * std::min(per_sm, 2);
 }
 
 static void precond_capture(Precond* K, cudaStream_t st) {
@@ -2626,9 +2466,7 @@ void precond_run(const Precond* K, double* z, const double* r, cudaStream_t st) 
   launch_fwd(v0, r, (nl > 1) ? K->lv[1].r : K->rc, (nl > 1) ? &K->lv[1] : nullptr, st);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   AJ_CUDA(cudaStreamIsCapturing(st, &cs));
-  if (K->tail_grid > 0) {
-    launch_tail(K, st);
-  } else if (K->exec && cs != cudaStreamCaptureStatusActive) {
+  if (K->exec && cs != cudaStreamCaptureStatusActive) {
     AJ_CUDA(cudaGraphLaunch(K->exec, st));
     g_launches += K->graph_nodes;
   } else {

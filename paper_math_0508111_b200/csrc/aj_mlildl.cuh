@@ -44,17 +44,6 @@ struct Level {
   void release(cudaStream_t st);
 };
 
-// device-side copy of the per-level pointers (persistent cooperative apply)
-struct LevelDesc {
-  int n, nF, nC, gf, gb;
-  const int32_t *cidx, *fidx, *partner;
-  const double *D, *b11, *b12;
-  const int64_t *Lptr, *LTptr;
-  const int32_t *Lcol, *LTcol;
-  const double *Lval, *LTval;
-  double *r, *z;
-};
-
 struct Precond {
   int L = 0, n0 = 0;
   aj_precond_params P{};
@@ -66,8 +55,6 @@ struct Precond {
   aj_precond_info info{};
   int64_t bytes_per_apply = 0;
   cudaGraphExec_t exec = nullptr;  // levels >= 1 + coarse, captured once
-  LevelDesc* dlv = nullptr;        // device level table for the cooperative apply
-  int tail_grid = 0;               // > 0: cooperative persistent apply of levels >= 1
   int64_t graph_nodes = 0;
 };
 

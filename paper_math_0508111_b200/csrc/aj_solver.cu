@@ -13,6 +13,7 @@
 // the preconditioner sweep, two tall-skinny dot kernels and one update kernel;
 // the host only reads the residual norm for the stopping test.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -246,36 +247,80 @@ __global__ void __launch_bounds__(256) k_small_eig(int j, int ldm, const double*
   for (int t = tid; t < j; t += blockDim.x) theta[t] = A[order[t]][order[t]];
 }
 
-__global__ void k_small_inv(int m, const double* __restrict__ H, double* __restrict__ Hinv, double* sc) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double A[17][34];
-  for (int a = 0; a < m; ++a)
-    for (int b = 0; b < 2 * m; ++b) A[a][b] = (b < m) ? 0.5 * (H[a + b * m] + H[b + a * m]) : (b - m == a ? 1.0 : 0.0);
+// Hinv = H^{-1} for the symmetrised m x m H (ld ldh), m <= 17, by Gauss-Jordan with
+// partial pivoting in one CTA: per column, warp 0 picks the pivot row (largest |a|,
+// smallest row on ties), then all threads swap, scale and eliminate.  A pivot with
+// |a| <= 1e-13 max|H| is a breakdown: *status = 1 and Hinv is not written (the caller
+// reads the status before using Hinv).
+constexpr int INV_MAX = 17;
+__global__ void __launch_bounds__(256)
+    k_small_inv(int m, const double* __restrict__ H, int ldh, double* __restrict__ Hinv, int* __restrict__ status) {
+  __shared__ double A[INV_MAX][2 * INV_MAX + 1];
+  __shared__ int s_piv;
+  __shared__ double s_thr;
+  const int tid = threadIdx.x, w = 2 * m;
+  for (int t = tid; t < m * w; t += blockDim.x) {
+    const int a = t / w, b = t % w;
+    A[a][b] = (b < m) ? 0.5 * (H[a + b * ldh] + H[b + a * ldh]) : (b - m == a ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double mx = 0.0;
+    for (int t = tid; t < m * m; t += 32) mx = fmax(mx, fabs(A[t / m][t % m]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (tid == 0) s_thr = 1e-13 * mx;
+  }
   for (int k = 0; k < m; ++k) {
-    int p = k;
-    for (int a = k + 1; a < m; ++a)
-      if (fabs(A[a][k]) > fabs(A[p][k])) p = a;
-    if (A[p][k] == 0.0) {
-      sc[S_BRK] = 2.0;
-      return;
+    __syncthreads();
+    if (tid < 32) {
+      const int a = k + tid;
+      double v = (a < m) ? fabs(A[a][k]) : -1.0;
+      int ix = (a < m) ? a : INT_MAX;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (v2 > v || (v2 == v && i2 < ix)) {
+          v = v2;
+          ix = i2;
+        }
+      }
+      if (tid == 0) s_piv = (v > s_thr) ? ix : -1;
+    }
+    __syncthreads();
+    const int p = s_piv;
+    if (p < 0) {
+      if (tid == 0) *status = 1;
+      return;  // uniform
     }
     if (p != k)
-      for (int b = 0; b < 2 * m; ++b) {
+      for (int b = tid; b < w; b += blockDim.x) {
         const double t = A[k][b];
         A[k][b] = A[p][b];
         A[p][b] = t;
       }
+    __syncthreads();
     const double inv = 1.0 / A[k][k];
-    for (int b = 0; b < 2 * m; ++b) A[k][b] *= inv;
-    for (int a = 0; a < m; ++a)
-      if (a != k) {
-        const double f = A[a][k];
-        if (f != 0.0)
-          for (int b = 0; b < 2 * m; ++b) A[a][b] -= f * A[k][b];
-      }
+    __syncthreads();
+    for (int b = tid; b < w; b += blockDim.x) A[k][b] *= inv;
+    __syncthreads();
+    // eliminate column k from the other rows; column k itself is read from a copy
+    double fa = 0.0;
+    if (tid < m) fa = A[tid][k];
+    __syncthreads();
+    __shared__ double fcol[INV_MAX];
+    if (tid < m) fcol[tid] = (tid == k) ? 0.0 : fa;
+    __syncthreads();
+    for (int t = tid; t < m * w; t += blockDim.x) {
+      const int a = t / w, b = t % w;
+      if (a != k && fcol[a] != 0.0) A[a][b] -= fcol[a] * A[k][b];
+    }
   }
-  for (int a = 0; a < m; ++a)
-    for (int b = 0; b < m; ++b) Hinv[a + b * m] = A[a][m + b];
+  __syncthreads();
+  for (int t = tid; t < m * m; t += blockDim.x) {
+    const int a = t % m, b = t / m;
+    Hinv[a + b * m] = A[a][m + b];
+  }
+  if (tid == 0) *status = 0;
 }
 
 // M[:, j] and M[j, :] <- dots (j+1 values)

@@ -33,6 +33,8 @@ def halo_exchange(x_ext, L, nz, group=None):
         return x_ext
     rank = dist.get_rank(group)
     down, up = (rank - 1) % world, (rank + 1) % world
+    if group is not None:  # P2POp peers are global ranks; down/up are ranks inside `group`
+        down, up = dist.get_global_rank(group, down), dist.get_global_rank(group, up)
     first, last = x_ext[P:2 * P], x_ext[nz * P:(nz + 1) * P]
     lo, hi = x_ext[:P], x_ext[(nz + 1) * P:(nz + 2) * P]
     # posting order matters when down == up (two ranks): messages between a pair are

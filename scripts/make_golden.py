@@ -42,6 +42,11 @@ def main(which):
                    normA_1=normA, method=method, oracle_seconds=dt,
                    source="scripts/make_golden.py -> oracle/ only")
         path = os.path.join(ROOT, "tests", "golden", f"eigs_config{c}.json")
+        if L > 14:
+            # eigenvectors of the k nearest pairs for the subspace-angle test (fp64, one column each)
+            vpath = os.path.join(ROOT, "tests", "golden", f"eigvecs_config{c}.npz")
+            np.savez_compressed(vpath, X=np.ascontiguousarray(X[:, :k].T))
+            out["eigenvectors"] = os.path.basename(vpath)
         with open(path, "w") as f:
             json.dump(out, f, indent=1)
         print(path, lam, dt)

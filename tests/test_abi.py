@@ -41,7 +41,7 @@ def test_argument_errors(lib):
     assert lib.anderson_build(ctypes.c_void_p(16), 2, 1.0, 1, None) == binding.AJ_ERR_ARG
     assert lib.spmv(None, None, None, 10, 1.0, 0.0, None) == binding.AJ_ERR_ARG
     assert lib.precond_apply(None, None, None, None) == binding.AJ_ERR_ARG
-    assert lib.precond_free(None) == binding.AJ_OK
+    assert lib.precond_free(None, None) == binding.AJ_OK
     # z-slab shard entry points: bounds checked before any device work
     assert lib.anderson_build_slab(ctypes.c_void_p(16), 10, 8, 3, 1.0, 1, None) == binding.AJ_ERR_ARG
     assert b"anderson_build_slab" in lib.aj_last_error()

@@ -410,26 +410,6 @@ def test_jd_host_e2e(gpu_lib):
         assert np.linalg.norm(r) <= 1e-8 * normA
 
 
-def test_precond_tail_paths_agree(gpu_lib, monkeypatch):
-    # the captured per-level graph (default) and the persistent cooperative apply
-    # (AJ_TAIL=1) implement the same operator
-    import torch
-    L = 24
-    eps = gpu_eps(gpu_lib, L, 16.5, 8)
-    r = T(rand_vec(L ** 3, 8))
-    p = gpu_lib.default_precond_params(factor_fp32=0)  # the cooperative path reads fp64 factors
-    K1 = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
-    monkeypatch.setenv("AJ_TAIL", "1")
-    K2 = gpu_lib.Precond(eps, L, -1.0, 0.0, p)
-    z1, z2 = torch.empty_like(r), torch.empty_like(r)
-    K1.apply(z1, r)
-    K2.apply(z2, r)
-    assert K1.info()["levels"] >= 3
-    assert torch.linalg.norm(z1 - z2) <= 1e-12 * torch.linalg.norm(z1)
-    K1.free()
-    K2.free()
-
-
 def test_jd_config2_l100_properties(gpu_lib):
     # BASELINE configs[2] at full size (n = 10^6): properties that hold at any size --
     # residuals recomputed with the oracle stencil, orthonormality, Rayleigh quotients,

@@ -36,14 +36,94 @@ def test_pair_d2_by_hand():
     dg, lmax1, d1, p = mlildl._pivot_quality(Ah)
     pairs = mlildl._pair_candidates(Ah, dg, lmax1, d1, p, kappa=5.0)
     assert len(pairs) == 1
-    i, j, B11, B12, B22, lm2 = pairs[0]
+    i, j, B11, B12, B22, lm2, d2 = pairs[0]
     assert (i, j) == (0, 1)
     det = 0.1 * 0.2 - 1.0
     assert np.isclose(B11, 0.2 / det) and np.isclose(B12, -1.0 / det) and np.isclose(B22, 0.1 / det)
     # rows c=2: (0.5, 0) B^{-1}; c=3: (0, 0.5) B^{-1}
-    # d2 = (0.5*0.2 + 0.5*1 + 0.5*1 + 0.5*0.1)/0.98, lmax2 = 0.6/0.98
-    assert np.isclose(lm2, 0.6 / 0.98)
+    # d2 = (0.5*0.2 + 0.5*1 + 0.5*1 + 0.5*0.1)/0.98, lmax2 = 0.6/0.98   (PAPER.md l.866-868:
+    # d2 = sum_{j>2} ||(s_j1, s_j2) B^{-1}||, the row norm read as the 1-norm, R8)
+    assert np.isclose(lm2, 0.6 / 0.98, rtol=0, atol=1e-15)
+    assert np.isclose(d2, 1.15 / 0.98, rtol=0, atol=1e-15)
+    # the paper's acceptance test d2 < d1 of the failing (leading) member 0: 1.173 < 15
+    dg, lmax1, d1, p = mlildl._pivot_quality(Ah)
+    assert d2 < d1[0]
 
+
+def _pair_star(m):
+    """Pair {0, 1}: a_00 = a_11 = 0.2, a_01 = 1 (both fail the 1x1 bound, lmax1 = 5);
+    node 1 also couples with 0.9 to m leaves (diagonal 1).  Unit row maxima: D = I."""
+    n = 2 + m
+    A = np.eye(n)
+    A[0, 0] = A[1, 1] = 0.2
+    A[0, 1] = A[1, 0] = 1.0
+    for c in range(2, n):
+        A[1, c] = A[c, 1] = 0.9
+    return A
+
+
+@pytest.mark.parametrize("m,accepted", [(3, True), (5, False)])
+def test_pair_d2_vs_d1_by_hand(m, accepted):
+    # PAPER.md l.874: "we perform a 2x2 update only if d2 < d1".  B^{-1} = [[0.2, -1], [-1, 0.2]] / -0.96;
+    # a leaf row (0, 0.9) B^{-1} has |l| = (0.9, 0.18)/0.96 -> 1.125 each: d2 = 1.125 m, lmax2 = 1.125;
+    # d1 of the leading (failing) member 0 = |a_10| / |a_00| = 5.  m = 3: 3.375 < 5 accepted;
+    # m = 5: 5.625 >= 5 rejected (then neither member is a pivot candidate)
+    A = _pair_star(m)
+    D, Ah = mlildl._scaled(sp.csr_matrix(A))
+    assert np.array_equal(D, np.ones(2 + m))
+    dg, lmax1, d1, p = mlildl._pivot_quality(Ah)
+    assert np.isclose(d1[0], 5.0) and list(p[:2]) == [1, 0]
+    pairs = mlildl._pair_candidates(Ah, dg, lmax1, d1, p, kappa=5.0)
+    assert (len(pairs) == 1) == accepted
+    if accepted:
+        i, j, B11, B12, B22, lm2, d2 = pairs[0]
+        assert np.isclose(d2, 1.125 * m, rtol=0, atol=1e-14) and np.isclose(lm2, 1.125, rtol=0, atol=1e-15)
+    # in the level, the leaves (lmax1 = 0.9 < lmax2) win the independent set either way and
+    # node 0 is never a 1x1 pivot: it is eliminated only as part of the accepted pair
+    Lv = mlildl.factor_level(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.02)
+    assert 0 not in Lv.F and Lv.npairs == 0
+
+def test_scaling_by_hand():
+    # reading R7 (PAPER.md l.805-807, "D is a diagonal matrix"): D_i = 1/sqrt(max_j |a_ij|),
+    # a^_ij = a_ij (D_i D_j).  Row maxima 4, 2, 0.25 -> D = (1/2, 1/sqrt 2, 2)
+    A = np.array([[4.0, -1.0, 0.1],
+                  [-1.0, 0.5, 2.0],
+                  [0.1, 2.0, 0.25]])
+    D, Ah = mlildl._scaled(sp.csr_matrix(A))
+    rowmax = np.abs(A).max(axis=1)
+    assert np.allclose(rowmax, [4.0, 2.0, 2.0])
+    assert np.allclose(D, [0.5, 1 / np.sqrt(2.0), 1 / np.sqrt(2.0)], rtol=0, atol=1e-16)
+    Ah_ref = np.array([[1.0, -1.0 / (2 * np.sqrt(2.0)), 0.1 / (2 * np.sqrt(2.0))],
+                       [-1.0 / (2 * np.sqrt(2.0)), 0.25, 1.0],
+                       [0.1 / (2 * np.sqrt(2.0)), 1.0, 0.125]])
+    assert np.allclose(Ah.toarray(), Ah_ref, rtol=0, atol=1e-15)
+    # every row of A^ has max |a^_ij| <= 1, attained where a_ij realises both row maxima
+    assert np.abs(Ah.toarray()).max() <= 1.0 + 1e-15
+
+
+def test_scaled_level_factor_by_hand():
+    # one level with non-unit scaling, values worked out by hand.  Row maxima 4, 2, 0.5:
+    # D = (1/2, 1/sqrt 2, sqrt 2); A^ = [[1, 1/(2 sqrt 2), 0], [., 1, 1/2], [0, 1/2, 1/2]].
+    # All three pass the 1x1 test (lmax1 = 0.354, 0.5, 1.0); no pair (both members of the
+    # mutual proposal {1, 2} pass).  The MIS on the strong graph (tau_strong = 0, ranked by
+    # lmax1) takes 0, removes 1, then takes 2: F = {0, 2}, C = {1}.
+    # L = (a^_10 / a^_00, a^_12 / a^_22) = (1/(2 sqrt 2), 1), S = 1 - 1/8 - 1/2 = 3/8.
+    A = np.array([[4.0, 1.0, 0.0],
+                  [1.0, 2.0, 0.5],
+                  [0.0, 0.5, 0.25]])
+    D, Ah = mlildl._scaled(sp.csr_matrix(A))
+    assert np.allclose(D, [0.5, 1 / np.sqrt(2.0), np.sqrt(2.0)], rtol=0, atol=1e-15)
+    Lv = mlildl.factor_level(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.0)
+    assert list(Lv.F) == [0, 2] and list(Lv.C) == [1]
+    assert np.allclose(Lv.L.toarray(), [[1 / (2 * np.sqrt(2.0)), 0.0, 1.0]], rtol=0, atol=1e-15)
+    assert np.allclose(Lv.S.toarray(), [[0.375]], rtol=0, atol=1e-15)
+    # the operator M^{-1} = D (L D~ L^T)^{-1} D with the dense coarse inverse of S is exact
+    # here (nothing dropped): M^{-1} = A^{-1}
+    M = mlildl.MultilevelILDL(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.0, n_coarse_max=1,
+                              stall_frac=0.0)
+    assert len(M.levels) == 1 and M.coarse_n == 1
+    r = np.array([1.0, -2.0, 0.5])
+    assert np.allclose(M.apply(r), np.linalg.solve(A, r), rtol=1e-14, atol=0)
 
 def test_level_schur_by_hand():
     # blocks {0,1} (key 0.612), {2} (0.5), {3} (0.5): MIS on the strong graph picks {2};
@@ -227,3 +307,94 @@ def test_compensation_adds_no_schur_fill():
     assert np.isclose(Ld[0, 0], 0.5, rtol=0, atol=1e-15)
     assert np.isclose(Ld[0, 1], 0.5 * -(e * (1.0 * 1.0)), rtol=0, atol=1e-15)
     assert np.isclose(Ld[1, 0], 0.6 * -(e * (1.0 * 1.0)), rtol=0, atol=1e-15)
+
+
+def _level_matrices(A, M):
+    """The matrix each level of M factored: A, then the Schur complement of the previous level."""
+    mats = [sp.csr_matrix(A)]
+    for Lv in M.levels[:-1]:
+        mats.append(Lv.S)
+    return mats
+
+
+@pytest.mark.parametrize("case", ["lattice", "random"])
+def test_F_independent_in_strong_graph(case):
+    # reading R9: F is an independent set of pivot blocks in the strong graph |a^_ij| >= tau_strong
+    # (level 0 on the lattice: the red sites, independent in the whole stencil graph)
+    if case == "lattice":
+        L = 10
+        A = an.matrix(L, an.disorder(L, 16.5, 3), hop=-1.0)
+        M = mlildl.MultilevelILDL(A, lattice_L=L, tau_drop=2e-3, tau_strong=0.05, n_coarse_max=100)
+    else:
+        A = _rand_sym_indef(400, 0.02, 5)
+        M = mlildl.MultilevelILDL(A, tau_drop=1e-3, tau_strong=0.05, n_coarse_max=20)
+    assert len(M.levels) >= 2
+    for lev, (Al, Lv) in enumerate(zip(_level_matrices(A, M), M.levels)):
+        D = Lv.D
+        Ah = sp.csr_matrix(sp.diags(D) @ Al @ sp.diags(D)).tocoo()
+        inF = Lv.inF
+        partner = Lv.partner
+        m = (Ah.row != Ah.col) & inF[Ah.row] & inF[Ah.col] & (partner[Ah.row] != Ah.col)
+        thr = 0.0 if (lev == 0 and case == "lattice") else 0.05
+        assert np.all(np.abs(Ah.data[m]) < thr) if thr > 0 else not m.any(), lev
+
+
+def _plain_level(Al, Lv, compensate):
+    """The plain definitions of one level (reading R17): with
+    B~^{-1} = B_d^{-1} + V (block pivots + virtual couplings),
+      L = A^_CF B~^{-1}
+      S = A^_CC - A^_CF B_d^{-1} A^_FC - P o (A^_CF V A^_FC),
+    P = the structural pattern of A^_CC + A^_CF B_d^{-1} A^_FC (no fill from V)."""
+    D = Lv.D
+    Ah = sp.csr_matrix(sp.diags(D) @ Al @ sp.diags(D))
+    F, C = Lv.F, Lv.C
+    n = Ah.shape[0]
+    Binv = Lv.Binv.toarray()
+    part = Lv.partner
+    Bd = np.zeros_like(Binv)
+    for f in F:
+        Bd[f, f] = Binv[f, f]
+        if part[f] >= 0:
+            Bd[f, part[f]] = Binv[f, part[f]]
+    V = Binv - Bd
+    if not compensate:
+        assert not V.any()
+    Ad = Ah.toarray()
+    ACF, AFC, ACC = Ad[np.ix_(C, F)], Ad[np.ix_(F, C)], Ad[np.ix_(C, C)]
+    Lp = ACF @ Binv[np.ix_(F, F)]
+    S1 = ACC - ACF @ Bd[np.ix_(F, F)] @ AFC
+    pattern = (np.abs(ACC) > 0) | ((np.abs(ACF) > 0).astype(float) @ (np.abs(Bd[np.ix_(F, F)]) > 0).astype(float)
+                                   @ (np.abs(AFC) > 0).astype(float) > 0) | np.eye(len(C), dtype=bool)
+    S = S1 - np.where(pattern, ACF @ V[np.ix_(F, F)] @ AFC, 0.0)
+    return Lp, S
+
+
+@pytest.mark.parametrize("case,compensate", [("lattice", True), ("lattice", False), ("random", True),
+                                             ("random", False), ("lattice12", True)])
+def test_ordered_accumulation_equals_plain_definition(case, compensate):
+    # The oracle accumulates L and S block by block in ascending key (the order the GPU
+    # reproduces bit for bit, DESIGN.md R10/R17).  Pin that ordered accumulation to the plain
+    # matrix definitions, with dropping disabled (tau_drop = 0) but a real strong threshold
+    # (tau_strong > 0: weak F-F couplings exist, so R17's virtual blocks are exercised).
+    if case.startswith("lattice"):
+        L = 12 if case == "lattice12" else 8
+        A = an.matrix(L, an.disorder(L, 16.5, 2), hop=-1.0)
+        M = mlildl.MultilevelILDL(A, lattice_L=L, tau_drop=0.0, tau_strong=0.05, n_coarse_max=60,
+                                  max_levels=4 if L == 12 else 200, compensate=compensate, tau_virtual=0.0)
+    else:
+        A = _rand_sym_indef(250, 0.03, 7)
+        M = mlildl.MultilevelILDL(A, tau_drop=0.0, tau_strong=0.05, n_coarse_max=30, compensate=compensate,
+                                  tau_virtual=0.0)
+    assert len(M.levels) >= 2
+    nvirt = 0
+    for Al, Lv in zip(_level_matrices(A, M), M.levels):
+        Lp, Sp = _plain_level(Al, Lv, compensate)
+        Lo = Lv.L.toarray()[:, Lv.F]
+        So = Lv.S.toarray()
+        scale_L = max(1.0, np.abs(Lp).max())
+        scale_S = max(1.0, np.abs(Sp).max())
+        assert np.abs(Lo - Lp).max() <= 1e-14 * scale_L
+        assert np.abs(So - Sp).max() <= 1e-14 * scale_S
+        # pattern: the oracle stores exactly the structural pattern (no entries outside it)
+        nvirt += Lv.nvirtual
+    assert (nvirt > 0) == compensate

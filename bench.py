@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--prof-cats", default="precond_apply,precond_setup",
                     help="phases timed live inside the timed region (each adds two stream events per call)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--large", default="3,4",
+                    help="BASELINE configs solved once each at full size on one GPU (driver-timed 'large' block)")
     # tuning knobs (defaults = library defaults, aj_*_default_params)
     for k in ["kappa", "tau_drop", "tau_strong", "inner_tol", "switch_tol"]:
         ap.add_argument("--" + k.replace("_", "-"), type=float, default=None)
@@ -147,55 +149,78 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-CPU_SAMPLE_L = 24
-
-
 def log(*a):
     print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
-def cpu_baseline(cfg, k, seed, Ls=CPU_SAMPLE_L):
-    """The oracle as it stands (numpy/scipy, 1 thread): one full solve (multilevel ILDL
-    setup + JD, same W, seed, sigma, tol, k) on a bounded L_s^3 sample of the workload,
-    scaled linearly in the number of sites to the workload's L^3."""
+def _oracle_solve(job):
+    """One full oracle solve (multilevel ILDL setup + JD, oracle/mlildl.py + oracle/jd.py,
+    numpy/scipy on 1 thread) of the workload `cfg`; returns (seconds, eigenvalues)."""
+    cfg, k, seed = job
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
     from threadpoolctl import threadpool_limits
 
     from oracle import anderson as an
     from oracle import mlildl
     from oracle.jd import jd_nearest
     L, W, hop, sigma, tol = cfg["L"], cfg["W"], cfg["hop"], cfg["sigma"], cfg["tol"]
-    Ls = min(Ls, L)
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
-        e = an.disorder(Ls, W, seed)
-        A = an.matrix(Ls, e, hop=hop)
-        M = mlildl.MultilevelILDL(an.matrix(Ls, e, hop=hop, sigma=sigma), lattice_L=Ls, n_coarse_max=1024)
+        e = an.disorder(L, W, seed)
+        A = an.matrix(L, e, hop=hop)
+        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=1024)
         lam, X, st = jd_nearest(A, M.apply, k, sigma=sigma, tol=tol)
         dt = time.perf_counter() - t0
-    scale = (L ** 3) / (Ls ** 3)
-    return dt * scale, dt, Ls, scale
+    return dt, [float(v) for v in lam]
+
+
+def cpu_baseline(cfg, k, seed):
+    """The oracle as it stands, timed on one host core: one full solve of the workload itself."""
+    dt, lam = _oracle_solve((cfg, k, seed))
+    return dt, lam
 
 
 def run_reference(args, cfg, ws, rank):
+    """--impl reference: the CPU oracle on the box's host cores.  K full solves of the
+    workload run concurrently on min(K, cores) worker processes (1 thread each); the timed
+    region is the wall time from submitting the K solves until the last one finishes, and
+    `value` = that time / K (the host's time per solved workload with all its cores busy).
+    Warm-up: W untimed solves of configs[0] (L=10) spread over the workers, which imports
+    numpy/scipy and the oracle in every worker process."""
     if rank != 0:
         return
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    from inputs import CONFIGS
     k = cfg["k"]
-    times = []
-    for i in range(args.warmup + args.steps):
-        dt, raw, Ls, scale = cpu_baseline(cfg, k, cfg["seed"])
-        log(f"reference step {i}: sample {raw:.1f}s x {scale:.2f}")
-        if i >= args.warmup:
-            times.append(dt)
-    v = sum(times) / len(times)
+    cores = os.cpu_count() or 1
+    P = max(1, min(args.steps, cores))
+    ctx = mp.get_context("fork")
+    with cf.ProcessPoolExecutor(max_workers=P, mp_context=ctx) as ex:
+        wcfg = CONFIGS[0]
+        list(ex.map(_oracle_solve, [(wcfg, wcfg["k"], wcfg["seed"])] * max(args.warmup, P)))
+        log(f"reference: warm-up done on {P} workers ({cores} host cores)")
+        t0 = time.perf_counter()
+        res = list(ex.map(_oracle_solve, [(cfg, k, cfg["seed"])] * args.steps))
+        wall = time.perf_counter() - t0
+    lat = [r[0] for r in res]
+    v = wall / args.steps
+    log(f"reference: {args.steps} solves in {wall:.1f} s on {P} workers; per-solve latency median "
+        f"{statistics.median(lat):.1f} s")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg),
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
-                             "sample": f"per step: one full oracle solve (oracle/jd.py + oracle/mlildl.py, numpy, 1 "
-                                       f"thread) on L={Ls} with the same W/seed/sigma/tol/k, scaled x{scale:.3f} "
-                                       f"(sites ratio) to L={cfg['L']}"},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": "s", "cores": P, "kind": "oracle",
+                             "sample": f"{args.steps} full oracle solves of this workload (oracle/mlildl.py setup + "
+                                       f"oracle/jd.py, numpy/scipy, 1 thread each) on {P} concurrent worker "
+                                       f"processes; value = wall time {wall:.1f} s / {args.steps}",
+                             "latency_s": {"median": statistics.median(lat), "min": min(lat), "max": max(lat)},
+                             "timed_wall_s": wall, "host_cores": cores},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "eigenvalues": res[0][1]}
     print(json.dumps(line), flush=True)
 
 
@@ -287,6 +312,55 @@ def big_roofline(binding, L, peak, Lp):
     return out
 
 
+def large_solve(binding, c, peak, pp, jp):
+    """One full-size solve of BASELINE configs[c] on this GPU (device-timed with CUDA
+    events), with the live per-phase throughput of the setup and of the preconditioner
+    apply inside it."""
+    import numpy as np
+    import torch
+
+    from inputs import CONFIGS
+    cfg = CONFIGS[c]
+    L, k = cfg["L"], cfg["k"]
+    n = L ** 3
+    eps = torch.empty(n, dtype=torch.float64, device="cuda")
+    binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
+    st = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    binding.prof_enable(True, categories=["precond_apply", "precond_setup", "spmv"])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    lam, X, res, stats = binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp,
+                                          want_vectors=True)
+    e1.record(st)
+    e1.synchronize()
+    prof = binding.prof_get()
+    binding.prof_enable(False)
+    normA = 6 * abs(cfg["hop"]) + float(eps.abs().max())
+    G = (X.T @ X).cpu().numpy()
+    pi = stats["precond"]
+    out = {"workload": f"configs[{c}]: L={L} (n={n}), W={cfg['W']}, seed {cfg['seed']}, {k} pairs nearest "
+                       f"sigma={cfg['sigma']}, tol {cfg['tol']}",
+           "time_to_solution_s": e0.elapsed_time(e1) / 1e3, "setup_ms": stats["setup_ms"],
+           "solve_ms": stats["solve_ms"], "outer": stats["outer"], "inner_total": stats["inner_total"],
+           "levels": pi["levels"], "coarse_n": pi["coarse_n"], "nnz_L_per_site": pi["nnz_L"] / n,
+           "max_resid_rel": float(np.max(res)) / normA, "orth_err": float(np.abs(G - np.eye(k)).max()),
+           "eigenvalues": [float(v) for v in lam],
+           "setup_work": {"schur_products": pi["setup_products"], "bytes_model": pi["setup_bytes"],
+                          "products_per_s": pi["setup_products"] / (stats["setup_ms"] * 1e-3),
+                          "GB/s_model": pi["setup_bytes"] / (stats["setup_ms"] * 1e-3) / 1e9,
+                          "frac_hbm": pi["setup_bytes"] / (stats["setup_ms"] * 1e-3) / 1e9 / peak}}
+    for cat in ("precond_apply", "spmv"):
+        v = prof[cat]
+        if v["calls"]:
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            out[cat] = {"calls": v["calls"], "ms_per_call": v["ms"] / v["calls"], "bytes_per_call":
+                        v["bytes"] / v["calls"], "GB/s": gbs, "frac": gbs / peak}
+    del eps, X
+    torch.cuda.empty_cache()
+    return out
+
+
 def replica_seed(cfg, rank):
     """N>1 (DESIGN.md sect. 6): one independent disorder realisation per rank."""
     return cfg["seed"] + rank
@@ -346,7 +420,7 @@ def run_ours(args, cfg, ws, rank, local):
     ms_step = allreduce_max(ws, total_ms / args.steps)
 
     # roofline of the dominant phase inside the timed region
-    cats = {c: v for c, v in prof.items() if c != "precond_setup" and v["calls"] > 0}
+    cats = {c: v for c, v in prof.items() if v["calls"] > 0 and v["bytes"] > 0}
     dom = max(cats, key=lambda c: cats[c]["ms"])
     d = cats[dom]
     avg_ms = d["ms"] / d["calls"]
@@ -354,6 +428,8 @@ def run_ours(args, cfg, ws, rank, local):
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": apply_traffic(L) if dom == "precond_apply" else None,
+            "bytes_model": "precond_apply: 12 B per stored factor entry + per-level vectors; precond_setup: 12 B x "
+                           "(level matrix + 2 FC lists + one FC entry per Schur product + 3 S + 4 L), DESIGN.md sect. 4",
             "traffic_source": "profiles/round1_apply_traffic.json (ncu dram__bytes_read+write, one apply)",
             "peak_source": peak_src,
             "avg_launch_ms": avg_ms, "bytes_per_launch": d["bytes"] / d["calls"],
@@ -396,15 +472,23 @@ def run_ours(args, cfg, ws, rank, local):
             kr = {"error": str(ex)[:300]}
 
     log(f"kernel roofline: {kr}")
+    large = None
+    if rank == 0 and ws == 1 and args.large:
+        large = {}
+        for c in [int(x) for x in args.large.split(",") if x.strip()]:
+            try:
+                large[f"configs[{c}]"] = large_solve(binding, c, peak, pp, jp)
+            except Exception as ex:  # report, do not hide
+                large[f"configs[{c}]"] = {"error": str(ex)[:300]}
+            log(f"large configs[{c}]: {large[f'configs[{c}]']}")
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        dt, raw, Ls, scale = cpu_baseline(cfg, k, seed)
+        dt, lam_o = cpu_baseline(cfg, k, seed)
         cpu = {"value": dt, "unit": "s", "cores": 1, "kind": "oracle",
-               "sample": f"one full oracle solve (oracle/jd.py + oracle/mlildl.py, numpy/scipy, 1 thread) on "
-                         f"L={Ls} (same W, seed, sigma, tol, k) took {raw:.2f} s; scaled x{scale:.3f} by the "
-                         f"sites ratio to L={L} (linear extrapolation; the oracle's per-site cost grows with L, "
-                         f"so this understates it)"}
-        log(f"cpu baseline: {raw:.1f} s sample")
+               "sample": f"one full oracle solve of this workload itself (L={L}: oracle/mlildl.py setup + "
+                         f"oracle/jd.py, numpy/scipy, 1 thread), {dt:.1f} s",
+               "eigenvalues": lam_o}
+        log(f"cpu baseline: {dt:.1f} s (L={L} oracle solve)")
 
     clocks = clk.summary()
     if rank == 0:
@@ -412,7 +496,7 @@ def run_ours(args, cfg, ws, rank, local):
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(cfg),
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline_clean(roof),
-                "cpu_baseline": cpu, "kernel_roofline": kr,
+                "cpu_baseline": cpu, "kernel_roofline": kr, "large": large,
                 "jd": {"outer": stats["outer"], "inner_total": stats["inner_total"],
                        "levels": stats["precond"]["levels"], "coarse_n": stats["precond"]["coarse_n"],
                        "setup_ms": stats["setup_ms"], "solve_ms": stats["solve_ms"],

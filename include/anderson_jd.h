@@ -131,6 +131,8 @@ typedef struct {
   double tau_strong;      /* resolved strong-coupling threshold                   */
   double tau_virtual;     /* resolved compensation threshold (0 if compensate=0)  */
   int64_t nnz_V;          /* virtual 2x2 blocks over all levels (R17)             */
+  int64_t setup_products; /* Schur products l_cx a_c'x over all levels (work model) */
+  double setup_bytes;     /* compulsory setup traffic model, bytes (DESIGN.md sect. 4) */
 } aj_precond_info;
 
 AJ_API void aj_precond_default_params(aj_precond_params* p);
@@ -211,6 +213,68 @@ AJ_API int jd_solve(int32_t k, double sigma, double tol, const double* d_eps, in
 AJ_API int jd_solve_host(int32_t k, double sigma, double tol, const double* h_eps, int32_t L, double hop,
                   const aj_precond_params* pparams, const aj_jd_params* jparams, double* h_lambda,
                   double* h_X, double* h_resid, aj_jd_stats* stats, void* stream);
+
+/* ------------------------------------------------------------------------- *
+ * z-slab sharded solve over `world` processes, one GPU each (row (e); north star:
+ * "The lattice shards naturally into z-slabs across 1/2/4/8 GPUs ... with one-plane
+ * halo exchange and dot-product allreduce via NCCL"; the paper's motivation is
+ * N = 10^6..10^8).  Rank r owns the planes
+ * z0 <= k < z0 + nz of the periodic L^3 lattice; its vectors are the nz L^2 sites of
+ * those planes (same site order as the full lattice, offset z0 L^2).  Every
+ * cross-rank step goes through an aj_comm:
+ *   allreduce   in-place sum (op 0) or max (op 1) of `count` doubles over the ranks,
+ *               ordered on `stream` (the fused dot products of SQMR/JD, <= 64 values);
+ *   halo_start  send this slab's first plane to rank-1 and its last plane to rank+1,
+ *               receive rank-1's last plane into d_recv_lo and rank+1's first plane into
+ *               d_recv_hi (periodic in z), ordered after prior work on `stream`;
+ *   halo_wait   orders `stream` after the receives (the interior planes of the SpMV
+ *               run in between).
+ * Callbacks return 0 on success.  The library provides an NCCL implementation
+ * (aj_comm_nccl_create); the binding provides a torch.distributed one (gloo on CPU
+ * tests).  A NULL comm or world == 1 means one process owns the periodic lattice.
+ * ------------------------------------------------------------------------- */
+typedef struct aj_comm {
+  int32_t world;
+  int32_t rank;
+  void* ctx;
+  int (*allreduce)(void* ctx, double* d_buf, int32_t count, int32_t op, void* stream);
+  int (*halo_start)(void* ctx, const double* d_send_lo, const double* d_send_hi, double* d_recv_lo,
+                    double* d_recv_hi, int64_t count, void* stream);
+  int (*halo_wait)(void* ctx, void* stream);
+} aj_comm;
+
+/* NCCL communicator of the sharded solve.  libnccl: path of the libnccl.so.2 to
+ * dlopen (NULL = the default search; pass the one torch.distributed loaded).
+ * aj_nccl_unique_id writes the 128-byte ncclUniqueId (rank 0 creates it, the
+ * caller broadcasts it); aj_comm_nccl_create: every rank, collective. */
+AJ_API int aj_nccl_unique_id(const char* libnccl, void* h_id);
+AJ_API int aj_comm_nccl_create(aj_comm** comm, const char* libnccl, const void* h_id, int32_t world, int32_t rank);
+AJ_API int aj_comm_nccl_free(aj_comm* comm);
+
+/* y = (A - sigma I) x on this rank's slab (the operator of spmv), the two halo
+ * planes exchanged through `comm` (overlapped with the interior planes).
+ * d_y, d_x, d_eps: device, nz L^2 doubles (d_eps from anderson_build_slab).
+ * Errors: AJ_ERR_ARG on bad sizes (nz >= 2 when comm->world > 1), AJ_ERR_CUDA if a
+ * callback fails. */
+AJ_API int spmv_sharded(double* d_y, const double* d_x, const double* d_eps, int32_t L, int32_t z0, int32_t nz,
+                        double hop, double sigma, const aj_comm* comm, void* stream);
+
+/* The multilevel ILDL of this rank's diagonal block of A - sigma I: the slab with
+ * periodic x, y and (for world > 1) open z faces -- block Jacobi over the slabs at the
+ * finest level, every level inside the slab (DESIGN.md sect. 6).  Level 0 is the red
+ * set of the GLOBAL lattice parity.  world == 1 reproduces precond_setup. */
+AJ_API int precond_setup_slab(void** handle, const double* d_eps, int32_t L, int32_t z0, int32_t nz, int32_t world,
+                              double hop, double sigma, const aj_precond_params* params, void* stream);
+
+/* jd_solve on the sharded lattice: same arguments and results as jd_solve, with
+ * d_eps (nz L^2, this rank's slab) and d_X (nz L^2 x k, this rank's part of the
+ * eigenvectors, may be NULL); h_lambda / h_resid are identical on every rank.  The
+ * preconditioner is precond_setup_slab of every rank (block Jacobi over slabs).
+ * Collective: every rank calls it with the same k, sigma, tol, params. */
+AJ_API int jd_solve_sharded(int32_t k, double sigma, double tol, const double* d_eps, int32_t L, int32_t z0,
+                            int32_t nz, double hop, const aj_precond_params* pparams, const aj_jd_params* jparams,
+                            double* h_lambda, double* d_X, double* h_resid, aj_jd_stats* stats, const aj_comm* comm,
+                            void* stream);
 
 /* Number of kernel launches issued by this thread since the last reset
  * (bench accounting of "gpu_launches"). */

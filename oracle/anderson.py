@@ -120,3 +120,16 @@ def red_sites(L):
     if L % 2 == 1:
         red &= (i < L - 1) & (j < L - 1) & (k < L - 1)
     return red
+
+
+def slab_rows(L, z0, nz):
+    """Sites of planes [z0, z0 + nz) (a z-slab shard, DESIGN.md sect. 6), ascending."""
+    return np.arange(z0 * L * L, (z0 + nz) * L * L)
+
+
+def slab_block(L, z0, nz, eps, hop=1.0, sigma=0.0):
+    """The diagonal block of A - sigma I on the planes of a slab: the block-Jacobi piece
+    of the sharded preconditioner (couplings to other slabs dropped; for nz = L the
+    whole periodic matrix).  eps: the full lattice."""
+    r = slab_rows(L, z0, nz)
+    return sp.csr_matrix(matrix(L, eps, hop=hop, sigma=sigma)[r][:, r])

@@ -166,7 +166,9 @@ def _mis(nb, keyrank, edges_a, edges_b):
 
 
 def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.005, compensate=True,
-                 tau_virtual=None, priority="quality"):
+                 tau_virtual=None, priority="quality", red=None):
+    """One level.  Level 0 of a lattice (lattice_L given, or an explicit `red` mask for a
+    z-slab block, DESIGN.md sect. 6) takes the red sites as its independent set."""
     n = A.shape[0]
     D, Ah = _scaled(A)
     dg, lmax1, d1, p = _pivot_quality(Ah)
@@ -176,7 +178,8 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
     partner = np.full(n, -1, dtype=np.int64)
     b11 = np.zeros(n)
     b12 = np.zeros(n)
-    if lattice_L is None:
+    lattice = lattice_L is not None or red is not None
+    if not lattice:
         pairs = _pair_candidates(Ah, dg, lmax1, d1, p, kappa)
     else:
         pairs = []
@@ -195,8 +198,8 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
         b11[singles] = 1.0 / dg[singles]
 
     # ---- independent set ------------------------------------------------------
-    if lattice_L is not None:
-        inF = singles & red_sites(lattice_L)
+    if lattice:
+        inF = singles & (red if red is not None else red_sites(lattice_L))
         rounds = 0
     else:
         blk = np.where(leader == np.arange(n))[0]           # block ids = leaders
@@ -281,8 +284,9 @@ def factor_level(A, kappa, tau_drop, tau_strong, lattice_L=None, stall_frac=0.00
     blocks = _blocks(Ah, inF, partner, b11, b12, compensate, tv)
     Lv.nvirtual = int((blocks["kind"] == 2).sum())
     inc = _incidence(Ah, inF, blocks)
-    Lv.L = _l_rows(inc, blocks, n, cmap, len(Lv.C), tau_drop)
-    Lv.S = _schur_blocks(Ah, inF, inc, blocks, Lv.C, cmap, tau_drop)
+    lt = _l_terms(inc, blocks, n)
+    Lv.L = _l_rows(lt, n, cmap, len(Lv.C), tau_drop)
+    Lv.S = _schur(Ah, inF, lt, Lv.C, cmap, tau_drop)
     Lv.Binv = _binv_blocks(n, blocks)
     return Lv
 
@@ -324,7 +328,8 @@ def _blocks(Ah, inF, partner, b11, b12, compensate, tau_virtual=0.0):
 
 def _incidence(Ah, inF, blk):
     """Elements (C row c, block b) for every block with a member adjacent to c:
-    a_cf, a_cg = a^ from c to the block's first / second member (0 if absent)."""
+    a_cf, a_cg = a^ from c to the block's first / second member (0 if absent),
+    hf, hg = whether that member is adjacent (structurally) to c."""
     n = Ah.shape[0]
     coo = Ah.tocoo()
     r, c, v = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
@@ -348,89 +353,132 @@ def _incidence(Ah, inF, blk):
     uk, inv = _unique_inverse(key)
     acf = np.zeros(len(uk))
     acg = np.zeros(len(uk))
+    hf = np.zeros(len(uk), bool)
+    hg = np.zeros(len(uk), bool)
     acf[inv[e_pos == 0]] = e_a[e_pos == 0]
     acg[inv[e_pos == 1]] = e_a[e_pos == 1]
-    return dict(c=uk // nb, b=uk % nb, acf=acf, acg=acg)
+    hf[inv[e_pos == 0]] = True
+    hg[inv[e_pos == 1]] = True
+    return dict(c=uk // nb, b=uk % nb, acf=acf, acg=acg, hf=hf, hg=hg)
 
 
-def _l_rows(inc, blk, n, cmap, nC, tau_drop):
-    """L = A^_CF B~^{-1}: l_cx = sum over blocks b containing x (ascending key) of
-    [(a_cf, a_cg) B_b]_x, accumulated from 0; |l| < tau_drop dropped."""
+def _l_terms(inc, blk, n):
+    """Split row factor L = A^_CF B~^{-1} = L^r + L^v (reading R17).
+    L^r (real blocks, B_d^{-1}): for every (c, real block b) the members x of b get
+      l^r_cf = a_cf B_ff + a_cg B_gf,  l^r_cg = a_cf B_fg + a_cg B_gg   (singles: a_cf B_ff),
+    one entry per (c, x) (structural: also when the value is 0).
+    L^v (virtual blocks {f, g}, B~^{-1}_fg = b'): for c adjacent to f, x = g gets a_cf b';
+    for c adjacent to g, x = f gets a_cg b'; l^v_cx = sum of its terms in ascending block key
+    from 0.  Returns the (c, x) entries of both with their values and flags."""
     b = inc["b"]
+    c = inc["c"]
+    kind = blk["kind"][b]
     f, g = blk["f"][b], blk["g"][b]
     Bff, Bfg, Bgg = blk["Bff"][b], blk["Bfg"][b], blk["Bgg"][b]
-    acf, acg = inc["acf"], inc["acg"]
+    acf, acg, hf, hg = inc["acf"], inc["acg"], inc["hf"], inc["hg"]
+    key = blk["key"][b]
+    real = kind != 2
     single = g < 0
+    pair = real & ~single
     vf = np.where(single, acf * Bff, acf * Bff + acg * Bfg)
     vg = acf * Bfg + acg * Bgg
-    rows = np.concatenate([inc["c"], inc["c"][~single]])
-    cols = np.concatenate([f, g[~single]])
-    vals = np.concatenate([vf, vg[~single]])
-    keys = np.concatenate([blk["key"][b], blk["key"][b][~single]])
-    o = np.lexsort((keys, cols, rows))
-    rows, cols, vals = rows[o], cols[o], vals[o]
-    rk = rows * n + cols
-    uk, inv = _unique_inverse(rk)
-    acc = np.zeros(len(uk))
-    np.add.at(acc, inv, vals)              # sequential in ascending block key
-    lr, lc = uk // n, uk % n
-    keep = np.abs(acc) >= tau_drop
-    L = sp.csr_matrix((acc[keep], (cmap[lr[keep]], lc[keep])), shape=(nC, n))
+    rc = np.concatenate([c[real], c[pair]])
+    rx = np.concatenate([f[real], g[pair]])
+    rv = np.concatenate([vf[real], vg[pair]])
+    virt = kind == 2
+    m1, m2 = virt & hf, virt & hg
+    vc = np.concatenate([c[m1], c[m2]])
+    vx = np.concatenate([g[m1], f[m2]])
+    vt = np.concatenate([acf[m1] * Bfg[m1], acg[m2] * Bfg[m2]])
+    vk = np.concatenate([key[m1], key[m2]])
+    o = np.lexsort((vk, vx, vc))                       # per (c, x): ascending block key
+    vc, vx, vt = vc[o], vx[o], vt[o]
+    vuk, vinv = _unique_inverse(vc * n + vx)
+    lv = np.zeros(len(vuk))
+    np.add.at(lv, vinv, vt)                            # sequential, in that order
+    rk = rc * n + rx
+    allk = _unique(np.concatenate([rk, vuk]))
+    Lr = np.zeros(len(allk))
+    Lvv = np.zeros(len(allk))
+    isr = np.zeros(len(allk), bool)
+    isv = np.zeros(len(allk), bool)
+    pr = np.searchsorted(allk, rk)
+    pv = np.searchsorted(allk, vuk)
+    Lr[pr] = rv
+    isr[pr] = True
+    Lvv[pv] = lv
+    isv[pv] = True
+    return dict(c=allk // n, x=allk % n, lr=Lr, lv=Lvv, real=isr, virt=isv)
+
+
+def _l_rows(lt, n, cmap, nC, tau_drop):
+    """L_cx = l^r_cx + l^v_cx (one rounding), |L| < tau_drop dropped."""
+    val = lt["lr"] + lt["lv"]
+    keep = np.abs(val) >= tau_drop
+    L = sp.csr_matrix((val[keep], (cmap[lt["c"][keep]], lt["x"][keep])), shape=(nC, n))
     L.sort_indices()
     return L
 
 
-def _schur_blocks(Ah, inF, inc, blk, C, cmap, tau_drop):
-    """S = A^_CC - A^_CF B~^{-1} A^_FC, readings R10/R17:
-    s_cc' = a^_cc' - sum_{blocks b adjacent to c and c', ascending key} T_b(c, c') with
-      1x1 {f}:      T = B_ff (a_cf a_c'f)
-      2-member:     T = (B_ff (a_cf a_c'f) + B_gg (a_cg a_c'g)) + B_fg ((a_cf a_c'g) + (a_cg a_c'f))
-    (symmetric in c, c' term by term), then off-diagonals |s| < tau_drop dropped.
-    Reading R17: the pattern of S is that of A^_CC and the real blocks' terms; the
-    virtual blocks' terms are subtracted after the real ones (ascending key) and only
-    on that pattern (the compensation creates no fill)."""
+def _schur(Ah, inF, lt, C, cmap, tau_drop):
+    """S = A^_CC - L^r A^_FC - P o (L^v A^_FC) (readings R10/R17),
+    upper triangle computed, lower triangle its mirror:
+    s_cc' starts at a^_cc'; then the real terms l^r_cx a^_c'x are subtracted for x ascending
+    (creating fill), then the virtual terms l^v_cx a^_c'x for x ascending, only on the
+    pattern P of A^_CC and the real terms; each term is the rounded product.  Off-diagonals
+    |s| < tau_drop are dropped.  (Pinned to the plain matrix definition in
+    tests/test_oracle_mlildl.py::test_ordered_accumulation_equals_plain_definition.)"""
     n = Ah.shape[0]
     nC = len(C)
+    Ah = sp.csr_matrix(Ah)
     coo = Ah.tocoo()
-    r, c, v = coo.row, coo.col, coo.data
-    ec, eb, acf, acg = inc["c"], inc["b"], inc["acf"], inc["acg"]
-    o = np.lexsort((ec, eb))                         # group elements by block
-    ec, eb, acf, acg = ec[o], eb[o], acf[o], acg[o]
-    if len(eb):
-        gstart = np.flatnonzero(np.r_[True, eb[1:] != eb[:-1]])
-        gcnt = np.diff(np.r_[gstart, len(eb)])
-    else:
-        gstart = np.zeros(0, np.int64)
-        gcnt = np.zeros(0, np.int64)
-    gid = np.repeat(np.arange(len(gstart)), gcnt)
-    reps = gcnt[gid]
-    a_idx = np.repeat(np.arange(len(eb)), reps)
-    before = np.repeat(np.cumsum(reps) - reps, reps)
-    b_idx = gstart[gid[a_idx]] + (np.arange(len(a_idx)) - before)
-    bb = eb[a_idx]
-    single = blk["g"][bb] < 0
-    Bff, Bfg, Bgg = blk["Bff"][bb], blk["Bfg"][bb], blk["Bgg"][bb]
-    A1, A2 = acf[a_idx], acf[b_idx]
-    G1, G2 = acg[a_idx], acg[b_idx]
-    T = Bff * (A1 * A2)
-    pm = ~single
-    T[pm] = (Bff[pm] * (A1[pm] * A2[pm]) + Bgg[pm] * (G1[pm] * G2[pm])) + \
-        Bfg[pm] * ((A1[pm] * G2[pm]) + (G1[pm] * A2[pm]))
-    tk = cmap[ec[a_idx]] * nC + cmap[ec[b_idx]]
-    mc = (~inF[r]) & (~inF[c])
-    k0 = cmap[r[mc]] * nC + cmap[c[mc]]
-    virt = blk["kind"][bb] == 2
-    keys = _unique(np.concatenate([k0, tk[~virt], np.arange(nC) * (nC + 1)]))
-    pos = np.minimum(np.searchsorted(keys, tk), max(len(keys) - 1, 0))
-    on = ~virt | (keys[pos] == tk)                   # virtual terms: pattern entries only
-    tk, T, bb, virt = tk[on], T[on], bb[on], virt[on]
+    r, cc, v = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
+    # FC(x): the coarse neighbours of each pivot x (structural)
+    mfc = inF[r] & ~inF[cc]
+    fr, fcol, fval = r[mfc], cmap[cc[mfc]], v[mfc]
+    o = np.lexsort((fcol, fr))
+    fr, fcol, fval = fr[o], fcol[o], fval[o]
+    start = np.searchsorted(fr, lt["x"], side="left")
+    stop = np.searchsorted(fr, lt["x"], side="right")
+    cnt = stop - start
+    rep = np.repeat(np.arange(len(lt["x"])), cnt)
+    off = np.arange(len(rep)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    idx = np.repeat(start, cnt) + off
+    tc = cmap[lt["c"][rep]]
+    tc2 = fcol[idx]
+    tx = lt["x"][rep]
+    a = fval[idx]
+    tk = tc * nC + tc2
+    realt = lt["real"][rep]
+    virtt = lt["virt"][rep]
+    mc = (~inF[r]) & (~inF[cc])
+    k0 = cmap[r[mc]] * nC + cmap[cc[mc]]
+    keys = _unique(np.concatenate([k0, tk[realt], np.arange(nC) * (nC + 1)]))
     sval = np.zeros(len(keys))
     sval[np.searchsorted(keys, k0)] = v[mc]
-    ot = np.lexsort((blk["key"][bb], virt, tk))      # per entry: real, then virtual; ascending key
-    np.subtract.at(sval, np.searchsorted(keys, tk[ot]), T[ot])
+    # real terms (all on the pattern by construction), then virtual terms on the pattern
+    pos_r = np.searchsorted(keys, tk[realt])
+    T_r = lt["lr"][rep][realt] * a[realt]
+    pv = np.minimum(np.searchsorted(keys, tk[virtt]), max(len(keys) - 1, 0))
+    onp = keys[pv] == tk[virtt] if len(keys) else np.zeros(int(virtt.sum()), bool)
+    pos_v = pv[onp]
+    T_v = (lt["lv"][rep][virtt] * a[virtt])[onp]
+    x_r, x_v = tx[realt], tx[virtt][onp]
+    pos = np.concatenate([pos_r, pos_v])
+    T = np.concatenate([T_r, T_v])
+    ps = np.concatenate([np.zeros(len(pos_r), np.int64), np.ones(len(pos_v), np.int64)])
+    xx = np.concatenate([x_r, x_v])
+    ot = np.lexsort((xx, ps, pos))                     # per entry: real then virtual, x ascending
+    np.subtract.at(sval, pos[ot], T[ot])
     sr, sc = keys // nC, keys % nC
-    keep = (sr == sc) | (np.abs(sval) >= tau_drop)
-    S = sp.csr_matrix((sval[keep], (sr[keep], sc[keep])), shape=(nC, nC))
+    # S is symmetric: its upper triangle (c <= c') is taken as computed in row c and
+    # mirrored, S = triu(S) + triu(S, 1)^T, so S is symmetric bit for bit (the rounded
+    # terms l_cx a_c'x are not symmetric in (c, c'))
+    keep = (sr == sc) | ((sr < sc) & (np.abs(sval) >= tau_drop))
+    ur, uc, uv = sr[keep], sc[keep], sval[keep]
+    off = ur != uc
+    S = sp.csr_matrix((np.concatenate([uv, uv[off]]), (np.concatenate([ur, uc[off]]), np.concatenate([uc, ur[off]]))),
+                      shape=(nC, nC))
     S.sort_indices()
     return S
 
@@ -476,8 +524,9 @@ class MultilevelILDL:
 
     def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
                  n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False,
-                 compensate=True, tau_virtual=None, priority="quality"):
-        """factor_fp32 (reading R16): the stored factor values are rounded to
+                 compensate=True, tau_virtual=None, priority="quality", red=None):
+        """red: level-0 independent set of a lattice block (default red_sites(lattice_L)).
+        factor_fp32 (reading R16): the stored factor values are rounded to
         IEEE binary32 -- forward entries as fl32(l_cf * D_f), backward entries as
         fl32(l_cf) -- and used in fp64 arithmetic, as on the GPU."""
         self.levels = []
@@ -489,7 +538,7 @@ class MultilevelILDL:
                 break
             Lv = factor_level(cur, kappa, tau_drop, tau_strong,
                               lattice_L if lev == 0 else None, stall_frac, compensate, tau_virtual,
-                              priority)
+                              priority, red if lev == 0 else None)
             if Lv is None:
                 break
             if self.factor_fp32:

@@ -41,13 +41,14 @@ class PrecondInfo(ctypes.Structure):
                 ("nnz_A", ctypes.c_int64), ("level_n", ctypes.c_int32 * 1024), ("level_nF", ctypes.c_int32 * 1024),
                 ("level_pairs", ctypes.c_int32 * 1024), ("level_nnzS", ctypes.c_int64 * 1024),
                 ("setup_ms", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
-                ("tau_virtual", ctypes.c_double), ("nnz_V", ctypes.c_int64)]
+                ("tau_virtual", ctypes.c_double), ("nnz_V", ctypes.c_int64), ("setup_products", ctypes.c_int64),
+                ("setup_bytes", ctypes.c_double)]
 
     def as_dict(self):
         nl = self.levels
         return dict(levels=nl, coarse_n=self.coarse_n, nnz_L=self.nnz_L, nnz_A=self.nnz_A,
                     tau_drop=self.tau_drop, tau_strong=self.tau_strong, tau_virtual=self.tau_virtual,
-                    nnz_V=self.nnz_V,
+                    nnz_V=self.nnz_V, setup_products=self.setup_products, setup_bytes=self.setup_bytes,
                     level_n=list(self.level_n[:nl]), level_nF=list(self.level_nF[:nl]),
                     level_pairs=list(self.level_pairs[:nl]), level_nnzS=list(self.level_nnzS[:nl]),
                     setup_ms=self.setup_ms)

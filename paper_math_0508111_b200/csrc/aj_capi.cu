@@ -166,8 +166,8 @@ int sqmr_solve(void* handle, double* d_x, const double* d_b, const double* d_eps
     double* Y = aj::dalloc<double>(n, st);   // holds w
     aj::SqmrResult r;
     try {
-      r = aj::sqmr_run((aj::Precond*)handle, d_eps, L, hop, sigma, Qt, Y, 0, nullptr, d_b, d_x, tol, maxit, ws,
-                       st);
+      r = aj::sqmr_run((aj::Precond*)handle, d_eps, aj::domain_full(L), hop, sigma, Qt, Y, 0, nullptr, d_b, d_x, tol,
+                       maxit, ws, st);
     } catch (...) {
       aj::dfree(Qt, st);
       aj::dfree(Y, st);
@@ -240,7 +240,7 @@ void aj_jd_default_params(aj_jd_params* p) {
   p->verbose = 0;
 }
 
-static int jd_common(int32_t k, double sigma, double tol, const double* d_eps, int32_t L, double hop,
+static int jd_common(int32_t k, double sigma, double tol, const double* d_eps, const aj::Domain& dom, double hop,
                      const aj_precond_params* pparams, const aj_jd_params* jparams, double* h_lambda, double* d_X,
                      double* h_resid, aj_jd_stats* stats, cudaStream_t st) {
   aj_precond_params pp;
@@ -255,7 +255,7 @@ static int jd_common(int32_t k, double sigma, double tol, const double* d_eps, i
     aj_jd_default_params(&jp);
   aj_precond_info pinfo;
   memset(&pinfo, 0, sizeof(pinfo));
-  aj::JdResult R = aj::jd_run(k, sigma, tol, d_eps, L, hop, pp, jp, h_lambda, d_X, h_resid, &pinfo, st);
+  aj::JdResult R = aj::jd_run(k, sigma, tol, d_eps, dom, hop, pp, jp, h_lambda, d_X, h_resid, &pinfo, st);
   if (stats) {
     stats->outer = R.outer;
     stats->inner_total = R.inner_total;
@@ -277,7 +277,8 @@ int jd_solve(int32_t k, double sigma, double tol, const double* d_eps, int32_t L
              double* h_resid, aj_jd_stats* stats, void* stream) {
   if (!d_eps || !h_lambda || L < 3 || k < 1) return fail(AJ_ERR_ARG, "jd_solve: bad arguments");
   return guarded("jd_solve", [&] {
-    return jd_common(k, sigma, tol, d_eps, L, hop, pparams, jparams, h_lambda, d_X, h_resid, stats, S(stream));
+    return jd_common(k, sigma, tol, d_eps, aj::domain_full(L), hop, pparams, jparams, h_lambda, d_X, h_resid, stats,
+                     S(stream));
   });
 }
 
@@ -293,7 +294,8 @@ int jd_solve_host(int32_t k, double sigma, double tol, const double* h_eps, int3
     int rc;
     try {
       AJ_CUDA(cudaMemcpyAsync(d_eps, h_eps, n * sizeof(double), cudaMemcpyHostToDevice, st));
-      rc = jd_common(k, sigma, tol, d_eps, L, hop, pparams, jparams, h_lambda, d_X, h_resid, stats, st);
+      rc = jd_common(k, sigma, tol, d_eps, aj::domain_full(L), hop, pparams, jparams, h_lambda, d_X, h_resid, stats,
+                     st);
       if (h_X && (rc == AJ_OK || rc == AJ_ERR_NOCONV))
         AJ_CUDA(cudaMemcpyAsync(h_X, d_X, n * k * sizeof(double), cudaMemcpyDeviceToHost, st));
       AJ_CUDA(cudaStreamSynchronize(st));
@@ -304,6 +306,68 @@ int jd_solve_host(int32_t k, double sigma, double tol, const double* h_eps, int3
     }
     aj::dfree(d_eps, st);
     aj::dfree(d_X, st);
+    return rc;
+  });
+}
+
+// ---- z-slab sharded solve (include/anderson_jd.h, DESIGN.md sect. 6) ----------------
+static bool slab_ok(int32_t L, int32_t z0, int32_t nz, const aj_comm* comm) {
+  if (L < 3 || z0 < 0 || nz < 1 || z0 + nz > L) return false;
+  if (comm && (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world)) return false;
+  if (comm && comm->world > 1 && (!comm->allreduce || !comm->halo_start || !comm->halo_wait || nz >= L)) return false;
+  if (!(comm && comm->world > 1) && (z0 != 0 || nz != L)) return false;  // one process owns the whole lattice
+  return true;
+}
+
+int spmv_sharded(double* d_y, const double* d_x, const double* d_eps, int32_t L, int32_t z0, int32_t nz, double hop,
+                 double sigma, const aj_comm* comm, void* stream) {
+  if (!d_y || !d_x || !d_eps || d_y == d_x || !slab_ok(L, z0, nz, comm))
+    return fail(AJ_ERR_ARG, "spmv_sharded: bad arguments");
+  return guarded("spmv_sharded", [&] {
+    cudaStream_t st = S(stream);
+    aj::Domain dom = aj::domain_slab(L, z0, nz, comm, st);
+    try {
+      aj::dom_spmv(dom, d_y, d_x, d_eps, hop, sigma, st);
+    } catch (...) {
+      aj::domain_release(dom, st);
+      throw;
+    }
+    aj::domain_release(dom, st);
+    return AJ_OK;
+  });
+}
+
+int precond_setup_slab(void** handle, const double* d_eps, int32_t L, int32_t z0, int32_t nz, int32_t world,
+                       double hop, double sigma, const aj_precond_params* params, void* stream) {
+  if (!handle || !d_eps || L < 3 || z0 < 0 || nz < 1 || z0 + nz > L || world < 1 || (world == 1 && nz != L) ||
+      (world > 1 && nz >= L))
+    return fail(AJ_ERR_ARG, "precond_setup_slab: bad arguments");
+  return guarded("precond_setup_slab", [&] {
+    aj_precond_params p;
+    if (params)
+      p = *params;
+    else
+      aj_precond_default_params(&p);
+    *handle = aj::precond_create_slab(d_eps, L, z0, nz, world > 1, hop, sigma, p, S(stream));
+    return AJ_OK;
+  });
+}
+
+int jd_solve_sharded(int32_t k, double sigma, double tol, const double* d_eps, int32_t L, int32_t z0, int32_t nz,
+                     double hop, const aj_precond_params* pparams, const aj_jd_params* jparams, double* h_lambda,
+                     double* d_X, double* h_resid, aj_jd_stats* stats, const aj_comm* comm, void* stream) {
+  if (!d_eps || !h_lambda || k < 1 || !slab_ok(L, z0, nz, comm)) return fail(AJ_ERR_ARG, "jd_solve_sharded: bad arguments");
+  return guarded("jd_solve_sharded", [&] {
+    cudaStream_t st = S(stream);
+    aj::Domain dom = aj::domain_slab(L, z0, nz, comm, st);
+    int rc;
+    try {
+      rc = jd_common(k, sigma, tol, d_eps, dom, hop, pparams, jparams, h_lambda, d_X, h_resid, stats, st);
+    } catch (...) {
+      aj::domain_release(dom, st);
+      throw;
+    }
+    aj::domain_release(dom, st);
     return rc;
   });
 }

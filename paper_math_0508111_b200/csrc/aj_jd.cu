@@ -21,7 +21,7 @@ __global__ void k_small_inv(int m, const double* H, int ldh, double* Hinv, int* 
 __global__ void k_set_mcol(double* M, int ldm, int j, const double* dots);
 __global__ void k_set_mdiag(double* M, int ldm, int cnt, const double* theta, int off);
 __global__ void k_resid(int64_t n, const double* Au, const double* u, const double* theta, double* r, RedBuf rb);
-__global__ void k_start(int64_t n, uint64_t key, double* v);
+__global__ void k_start(int64_t n, uint64_t key, double* v, int64_t s0);
 __global__ void k_absmax(int64_t n, const double* x, unsigned long long* out);
 __global__ void k_negate_proj(int64_t n, double* b, const double* r, const double* Qt, int m, const double* c);
 
@@ -33,15 +33,16 @@ static void rd(T* h, const T* d, size_t cnt, cudaStream_t st) {
   AJ_CUDA(cudaStreamSynchronize(st));
 }
 
-JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, double hop,
+JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain& dom, double hop,
                 const aj_precond_params& pp, const aj_jd_params& jp, double* h_lambda, double* d_X,
                 double* h_resid, aj_precond_info* pinfo, cudaStream_t st) {
+  const int L = dom.L;
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "jd_solve: L must be >= 3");
   AJ_REQUIRE(k >= 1 && k <= 16, AJ_ERR_ARG, "jd_solve: 1 <= k <= 16");  // m = k + 1 <= 17 (k_small_inv)
   AJ_REQUIRE(jp.jmax <= 48 && jp.jmin >= 1 && jp.jmin < jp.jmax && jp.jmax >= 2, AJ_ERR_ARG,
              "jd_solve: need 1 <= jmin < jmax <= 48");
   AJ_REQUIRE(tol > 0.0 && h_lambda, AJ_ERR_ARG, "jd_solve: tol > 0 and h_lambda required");
-  const int64_t n = (int64_t)L * L * L;
+  const int64_t n = dom.n;
   AJ_REQUIRE((int64_t)k + 2 <= n && jp.jmax < n, AJ_ERR_ARG, "jd_solve: lattice too small for k / jmax");
   JdResult R;
   cudaEvent_t e0, e1, e2;
@@ -50,7 +51,9 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
   AJ_CUDA(cudaEventCreate(&e2));
   AJ_CUDA(cudaEventRecord(e0, st));
 
-  Precond* K = precond_create(eps, L, hop, sigma, pp, st);
+  // sharded: block Jacobi over the z-slabs (each rank factors its slab's diagonal block)
+  Precond* K = dom.sharded() ? precond_create_slab(eps, L, dom.z0, dom.nz, true, hop, sigma, pp, st)
+                             : precond_create(eps, L, hop, sigma, pp, st);
   if (pinfo) *pinfo = K->info;
   AJ_CUDA(cudaEventRecord(e1, st));
   Workspace ws(n, st);
@@ -92,6 +95,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
     AJ_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long), st));
     k_absmax<<<sg(n), 256, 0, st>>>(n, eps, amax);
     AJ_LAUNCHED();
+    dom_allreduce(dom, reinterpret_cast<double*>(amax), 1, 1, st);  // max |eps| (bit patterns of doubles >= 0)
     unsigned long long hm;
     rd(&hm, amax, 1, st);
     double emax;
@@ -99,7 +103,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
     const double normA = 6.0 * fabs(hop) + emax;  // ||A||_1
     const double tol_abs = tol * normA;
     uint64_t key = mix64(jp.seed ^ 0x4A44535441525431ull);
-    k_start<<<sg(n), 256, 0, st>>>(n, key, z);
+    k_start<<<sg(n), 256, 0, st>>>(n, key, z, dom.site0());
     AJ_LAUNCHED();
     int j = 0, nq = 0;
     double theta0 = 0.0, rnorm = 0.0;
@@ -109,31 +113,36 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
       double zn2 = 0.0;
       for (int attempt = 0;; ++attempt) {
         launch_dot(nrm, z, z, n, ws.rs, st);
+        dom_allreduce(dom, nrm, 1, 0, st);
         double before;
         rd(&before, nrm, 1, st);
         for (int pass = 0; pass < 2; ++pass) {
           if (nq > 0) {
             launch_multi_dot(cq, QT, nq, n, z, n, ws.rs, st);
+            dom_allreduce(dom, cq, nq, 0, st);
             launch_gemv(z, 1.0, -1.0, QT, nq, n, cq, n, st);
           }
           if (j > 0) {
             launch_multi_dot(cv, V, j, n, z, n, ws.rs, st);
+            dom_allreduce(dom, cv, j, 0, st);
             launch_gemv(z, 1.0, -1.0, V, j, n, cv, n, st);
           }
         }
         launch_dot(nrm, z, z, n, ws.rs, st);
+        dom_allreduce(dom, nrm, 1, 0, st);
         rd(&zn2, nrm, 1, st);
         if (std::isfinite(zn2) && zn2 > 1e-20 * std::max(before, 1e-300)) break;
         AJ_REQUIRE(attempt < 8, AJ_ERR_BREAKDOWN, "jd_solve: cannot extend the search space");
         key = mix64(key + 0x9E3779B97F4A7C15ull);
-        k_start<<<sg(n), 256, 0, st>>>(n, key, z);  // correction in span: random restart vector
+        k_start<<<sg(n), 256, 0, st>>>(n, key, z, dom.site0());  // correction in span: random restart vector
         AJ_LAUNCHED();
       }
       double* vj = V + (int64_t)j * n;
       launch_copy(vj, z, n, st);
       launch_normalize(vj, nrm, n, st);
-      launch_spmv(AV + (int64_t)j * n, vj, eps, L, hop, sigma, st);
+      dom_spmv(dom, AV + (int64_t)j * n, vj, eps, hop, sigma, st);
       launch_multi_dot(mcol, V, j + 1, n, AV + (int64_t)j * n, n, ws.rs, st);
+      dom_allreduce(dom, mcol, j + 1, 0, st);
       k_set_mcol<<<1, 64, 0, st>>>(M, jmax, j, mcol);
       AJ_LAUNCHED();
       ++j;
@@ -146,6 +155,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
         launch_gemv(Au, 0.0, 1.0, AV, j, n, S, n, st);
         k_resid<<<sg(n), 256, 0, st>>>(n, Au, u, theta, r, ws.rs.buf(rn2));
         AJ_LAUNCHED();
+        dom_allreduce(dom, rn2, 1, 0, st);
         double h2[2];
         AJ_CUDA(cudaMemcpyAsync(&h2[0], theta, sizeof(double), cudaMemcpyDeviceToHost, st));
         AJ_CUDA(cudaMemcpyAsync(&h2[1], rn2, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -181,7 +191,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
       if (done) break;
       if (need_new_start) {
         key = mix64(key + 0x9E3779B97F4A7C15ull);
-        k_start<<<sg(n), 256, 0, st>>>(n, key, z);
+        k_start<<<sg(n), 256, 0, st>>>(n, key, z, dom.site0());
         AJ_LAUNCHED();
         continue;
       }
@@ -205,6 +215,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
       launch_copy(QT + (int64_t)nq * n, u, n, st);
       precond_run(K, Y + (int64_t)nq * n, u, st);
       for (int c = 0; c < m; ++c) launch_multi_dot(Hb + c * mpad, QT, m, n, Y + (int64_t)c * n, n, ws.rs, st);
+      dom_allreduce(dom, Hb, m * mpad, 0, st);
       // Hinv = H^{-1} (H column c at Hb + c * mpad); a singular H (K^{-1} Q~ losing rank)
       // is reported, never silently replaced by the previous outer iteration's Hinv
       k_small_inv<<<1, 256, 0, st>>>(m, Hb, mpad, Hinv, hstat);
@@ -218,9 +229,10 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
       }
       const double shift = (rnorm < jp.switch_tol * normA) ? theta0 : 0.0;
       launch_multi_dot(cq, QT, m, n, r, n, ws.rs, st);
+      dom_allreduce(dom, cq, m, 0, st);
       k_negate_proj<<<sg(n), 256, 0, st>>>(n, b, r, QT, m, cq);
       AJ_LAUNCHED();
-      SqmrResult sr = sqmr_run(K, eps, L, hop, sigma + shift, QT, Y, m, Hinv, b, z, jp.inner_tol, jp.inner_max,
+      SqmrResult sr = sqmr_run(K, eps, dom, hop, sigma + shift, QT, Y, m, Hinv, b, z, jp.inner_tol, jp.inner_max,
                                ws, st);
       R.inner_total += sr.iters;
       ++R.outer;
@@ -233,8 +245,9 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, doubl
     for (int i = 0; i < nq; ++i) h_lambda[i] = lam[i];
     if (h_resid) {
       for (int i = 0; i < nq; ++i) {
-        launch_spmv(Au, QT + (int64_t)i * n, eps, L, hop, lam[i], st);
+        dom_spmv(dom, Au, QT + (int64_t)i * n, eps, hop, lam[i], st);
         launch_dot(nrm, Au, Au, n, ws.rs, st);
+        dom_allreduce(dom, nrm, 1, 0, st);
         double v;
         rd(&v, nrm, 1, st);
         h_resid[i] = sqrt(v);

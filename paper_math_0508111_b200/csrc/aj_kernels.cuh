@@ -36,6 +36,29 @@ void launch_disorder_slab(double* eps, int L, int z0, int nz, double W, uint64_t
 void launch_spmv_slab(double* y, const double* x_ext, const double* eps, int L, int nz, double hop, double sig,
                       cudaStream_t st);
 
+// --- the lattice a process works on (aj_stencil.cu): the whole periodic lattice, or
+//     one z-slab of a lattice sharded over comm->world processes (DESIGN.md sect. 6)
+struct Domain {
+  int L = 0, z0 = 0, nz = 0;
+  int64_t n = 0;                  // local sites L^2 nz
+  const aj_comm* comm = nullptr;  // null (or world == 1): this process owns the periodic lattice
+  double* halo = nullptr;         // sharded: 2 L^2 receive planes [below | above] (device)
+  bool sharded() const { return comm != nullptr && comm->world > 1; }
+  int64_t site0() const { return (int64_t)z0 * L * L; }
+};
+Domain domain_full(int L);
+// sharded domain; allocates the halo planes (release with domain_release)
+Domain domain_slab(int L, int z0, int nz, const aj_comm* comm, cudaStream_t st);
+void domain_release(Domain& d, cudaStream_t st);
+// in-place reduction over the ranks (op 0 sum, 1 max); no-op unless sharded
+void dom_allreduce(const Domain& d, double* buf, int count, int op, cudaStream_t st);
+// y = (A - sig I) x on the domain (halo exchange overlapped with the interior planes)
+void dom_spmv(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+              cudaStream_t st);
+// ... and out[c] = <y, W_c> (c < nv) over all ranks, via rb (rb.out: >= 2 nv doubles when sharded)
+void dom_spmv_dots(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+                   const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st);
+
 // --- tall skinny (aj_blas.cu) ---
 // out[0..m) = V^T x   (out device, padded to a multiple of 8)
 void launch_multi_dot(double* out, const double* V, int m, int64_t ld, const double* x, int64_t n,

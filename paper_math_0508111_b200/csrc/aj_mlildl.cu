@@ -27,6 +27,7 @@
 #include "aj_common.cuh"
 #include "aj_kernels.cuh"
 #include "aj_mlildl.cuh"
+#include "aj_sparse.cuh"
 
 namespace aj {
 
@@ -63,22 +64,30 @@ static int grid_sg(int64_t rows) { return std::max(1, std::min(ceil_div(rows * S
 
 
 // ----------------------------------------------------------------------------
-// level-0 CSR of A - sigma I on the lattice (7 sorted entries per row)
-__global__ void k_lattice_csr(int L, const double* __restrict__ eps, double hop, double sigma,
-                              int64_t* __restrict__ ptr, int32_t* __restrict__ col,
-                              double* __restrict__ val) {
-  const int64_t n = (int64_t)L * L * L;
+// level-0 CSR of A - sigma I on planes [z0, z0 + nz) of the lattice, periodic in x and y;
+// in z periodic inside the block (open_z = 0: the whole lattice, nz = L) or with open
+// faces (open_z = 1: a slab's diagonal block, couplings across the faces dropped).
+// Sorted rows of 7 (interior), 6 (face planes) or 5 (nz = 1) entries.
+__global__ void k_lattice_csr(int L, int nz, int open_z, const double* __restrict__ eps, double hop, double sigma,
+                              int64_t* __restrict__ ptr, int32_t* __restrict__ col, double* __restrict__ val) {
+  const int64_t P = (int64_t)L * L, n = P * nz;
   for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB) {
-    const int i = (int)(s % L), j = (int)((s / L) % L), k = (int)(s / ((int64_t)L * L));
+    const int i = (int)(s % L), j = (int)((s / L) % L), k = (int)(s / P);
+    const bool dn = !open_z || k > 0, up = !open_z || k < nz - 1;
+    auto len = [&](int kk) { return 5 + ((!open_z || kk > 0) ? 1 : 0) + ((!open_z || kk < nz - 1) ? 1 : 0); };
+    // rows before plane k: plane 0 has len(0) entries per row, the interior planes 7
+    const int64_t base = (k == 0) ? 0 : P * (int64_t)len(0) + P * 7 * (int64_t)(k - 1);
+    const int64_t p0 = base + (s - (int64_t)k * P) * len(k);
     int32_t c[7];
-    c[0] = (int32_t)s;
-    c[1] = (int32_t)(((i + L - 1) % L) + (int64_t)L * (j + (int64_t)L * k));
-    c[2] = (int32_t)(((i + 1) % L) + (int64_t)L * (j + (int64_t)L * k));
-    c[3] = (int32_t)(i + (int64_t)L * (((j + L - 1) % L) + (int64_t)L * k));
-    c[4] = (int32_t)(i + (int64_t)L * (((j + 1) % L) + (int64_t)L * k));
-    c[5] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + L - 1) % L)));
-    c[6] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + 1) % L)));
-    for (int a = 1; a < 7; ++a) {  // insertion sort
+    int m = 0;
+    c[m++] = (int32_t)s;
+    c[m++] = (int32_t)(((i + L - 1) % L) + (int64_t)L * (j + (int64_t)L * k));
+    c[m++] = (int32_t)(((i + 1) % L) + (int64_t)L * (j + (int64_t)L * k));
+    c[m++] = (int32_t)(i + (int64_t)L * (((j + L - 1) % L) + (int64_t)L * k));
+    c[m++] = (int32_t)(i + (int64_t)L * (((j + 1) % L) + (int64_t)L * k));
+    if (dn) c[m++] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + nz - 1) % nz)));
+    if (up) c[m++] = (int32_t)(i + (int64_t)L * (j + (int64_t)L * ((k + 1) % nz)));
+    for (int a = 1; a < m; ++a) {  // insertion sort
       int32_t v = c[a];
       int b = a - 1;
       while (b >= 0 && c[b] > v) {
@@ -87,11 +96,11 @@ __global__ void k_lattice_csr(int L, const double* __restrict__ eps, double hop,
       }
       c[b + 1] = v;
     }
-    ptr[s] = 7 * s;
-    if (s == n - 1) ptr[n] = 7 * n;
-    for (int a = 0; a < 7; ++a) {
-      col[7 * s + a] = c[a];
-      val[7 * s + a] = (c[a] == (int32_t)s) ? (eps[s] - sigma) : hop;
+    ptr[s] = p0;
+    if (s == n - 1) ptr[n] = p0 + m;
+    for (int a = 0; a < m; ++a) {
+      col[p0 + a] = c[a];
+      val[p0 + a] = (c[a] == (int32_t)s) ? (eps[s] - sigma) : hop;
     }
   }
 }
@@ -163,41 +172,6 @@ __global__ void k_scaled_quality(int n, const int64_t* __restrict__ ptr, const i
   }
 }
 
-// position of column `key` in the sorted row [lo,hi), or -1
-__device__ __forceinline__ int64_t lookup_idx(const int32_t* __restrict__ col, int64_t lo, int64_t hi,
-                                              int32_t key) {
-  int64_t a = lo, b = hi;
-  while (a < b) {
-    int64_t mid = (a + b) >> 1;
-    if (col[mid] < key)
-      a = mid + 1;
-    else
-      b = mid;
-  }
-  return (a < hi && col[a] == key) ? a : -1;
-}
-
-// returns a^_{row,key} or 0 (sorted row [lo,hi))
-__device__ __forceinline__ double lookup(const int32_t* __restrict__ col, const double* __restrict__ ah,
-                                         int64_t lo, int64_t hi, int32_t key) {
-  int64_t a = lo, b = hi;
-  while (a < b) {
-    int64_t mid = (a + b) >> 1;
-    if (col[mid] < key)
-      a = mid + 1;
-    else
-      b = mid;
-  }
-  return (a < hi && col[a] == key) ? ah[a] : 0.0;
-}
-
-// l_cu for member u of a block {f} or {f, g} (f < g) from the row values
-// a_cf, a_cg (0 if absent): l_cu = sum_{v in block, ascending} a_cv * Binv[v,u]
-// (the summation order of oracle/mlildl.py's sparse product).
-__device__ __forceinline__ double lval_pair(double a_cf, double a_cg, double Bvu_f, double Bvu_g) {
-  return __dadd_rn(__dmul_rn(a_cf, Bvu_f), __dmul_rn(a_cg, Bvu_g));
-}
-
 // (ii-a) 2x2 candidates: mutual strongest-neighbour proposals (sect. 6.2), d2 < d1_lead
 // and lmax2 <= kappa - 1 (sect. 7.2).  Thread i handles the pair {i, p(i)} when i < p(i).
 __global__ void k_pairs(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
@@ -247,7 +221,7 @@ __global__ void k_pairs(int n, const int64_t* __restrict__ ptr, const int32_t* _
 }
 
 // (ii-b) blocks: singles (ok1, unpaired) and pair leaders; red-set selection on level 0
-__global__ void k_blocks(int n, int L, const int8_t* __restrict__ ok1, const double* __restrict__ dg,
+__global__ void k_blocks(int n, int L, int z0, const int8_t* __restrict__ ok1, const double* __restrict__ dg,
                          const double* __restrict__ lmax1, const int32_t* __restrict__ partner,
                          int32_t* __restrict__ leader, double* __restrict__ q, double* __restrict__ b11,
                          int8_t* __restrict__ inF) {
@@ -262,8 +236,8 @@ __global__ void k_blocks(int n, int L, const int8_t* __restrict__ ok1, const dou
     } else {
       leader[i] = -1;
     }
-    if (L > 0) {  // level 0: red sites of the bipartite split (reading R6)
-      const int x = i % L, y = (i / L) % L, z = i / (L * L);
+    if (L > 0) {  // level 0: red sites of the bipartite split (reading R6), global parity
+      const int x = i % L, y = (i / L) % L, z = z0 + i / (L * L);
       bool red = ((x + y + z) & 1) == 0;
       if (L & 1) red = red && x < L - 1 && y < L - 1 && z < L - 1;
       inF[i] = (p < 0 && ok1[i] && red) ? 1 : 0;
@@ -515,817 +489,6 @@ __global__ void k_virtual(int n, const int64_t* __restrict__ ptr, const int32_t*
 
 __global__ void k_iota(int n, int32_t* __restrict__ out) {
   for (int i = blockIdx.x * TB + threadIdx.x; i < n; i += gridDim.x * TB) out[i] = i;
-}
-
-constexpr int SW = 4;            // warps per CTA
-constexpr int BMAX = 1024;       // F blocks (real + virtual) adjacent to one row (shared-memory variant)
-constexpr int HT = 2048;         // per-warp hash table, shared-memory variant (power of 2)
-constexpr int HTG = 32768;       // per-warp hash table, global-memory fallback variant
-constexpr int BMAXG = 2048;      // block list of the fallback variant
-struct BlkEnt {
-  int32_t f, g, lead;
-  int64_t key;  // (kmin << 32) | kmax: real block (leader, leader), virtual block (u, v)
-  double acf, acg, Bff, Bgg, Bfg;
-};
-constexpr size_t kSchurSmem = (size_t)SW * HT * (sizeof(int32_t) + sizeof(double));  // 2 CTAs per SM
-// global scratch per warp: list/keys (T int32) + values (T doubles) [+ table for the
-// fallback] + the block list and its key order
-template <int T, bool GLOBAL>
-constexpr size_t schur_scratch_words() {
-  return (size_t)T * (GLOBAL ? 6 : 3) + (size_t)(GLOBAL ? BMAXG : BMAX) * (sizeof(BlkEnt) / 4 + 1);
-}
-
-// bitonic sort of (key, value) pairs by key, one warp
-__device__ __forceinline__ void warp_bitonic_sort_kv(int32_t* a, double* v, int P) {
-  const int lane = threadIdx.x & 31;
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < P; t += 32) {
-        const int ixj = t ^ j;
-        if (ixj > t) {
-          const int32_t x = a[t], y = a[ixj];
-          const bool up = (t & k) == 0;
-          if ((x > y) == up) {
-            a[t] = y;
-            a[ixj] = x;
-            const double tv = v[t];
-            v[t] = v[ixj];
-            v[ixj] = tv;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
-constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
-
-// find-or-insert `key` into a table of size T (power of 2); returns the slot, or
-// -1 once the table holds 3T/4 keys (the row is then handed to the next tier; the
-// load cap keeps probe chains short).  New keys get value 0 and their slot
-// appended to `list`.
-template <int T>
-__device__ __forceinline__ int hslot(int32_t* tab, double* val, int32_t key, int* cnt, int32_t* list) {
-  constexpr int BITS = ilog2c(T);
-  static_assert((T & (T - 1)) == 0, "table size");
-  uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
-  for (int probe = 0; probe < T; ++probe) {
-    const int32_t prev = atomicCAS(&tab[h], -1, key);
-    if (prev == -1) {
-      val[h] = 0.0;
-      const int pos = atomicAdd(cnt, 1);
-      if (pos < T) list[pos] = (int32_t)h;
-      return pos < (T * 3) / 4 ? (int)h : -1;
-    }
-    if (prev == key) return (int)h;
-    h = (h + 1) & (T - 1);
-  }
-  return -1;
-}
-
-// slot of `key` in a warp's table, or -1 if absent (no insertion)
-template <int T>
-__device__ __forceinline__ int hfind(const int32_t* tab, int32_t key) {
-  constexpr int BITS = ilog2c(T);
-  uint32_t h = ((uint32_t)key * 2654435761u) >> (32 - BITS);
-  for (int probe = 0; probe < T; ++probe) {
-    const int32_t k = tab[h];
-    if (k == key) return (int)h;
-    if (k == -1) return -1;
-    h = (h + 1) & (T - 1);
-  }
-  return -1;
-}
-
-// Schur complement S = A^_CC - A^_CF B^{-1} A^_FC, scatter form (reading R10):
-// s_cc' starts at a^_cc', then the F blocks adjacent to c are applied one after
-// the other in ascending leader order; block b walks the rows of its members and
-// subtracts T_b(c, c') from the slot of every coarse neighbour c' (each c' once
-// per block, so lanes never share a slot inside a block).  The per-entry order
-// is ascending leader -- the oracle's order, bitwise symmetric in (c, c').
-// Off-diagonals |s| < tau are dropped.  One warp per coarse row.
-// GLOBAL = false: tables in shared memory (T = 2048); rows that do not fit are
-// flagged in row_ovf and queued in ovf_list.  GLOBAL = true: the fallback over
-// ovf_list with T = 32768 tables in global memory.
-template <bool GLOBAL>
-__global__ void __launch_bounds__(SW * 32, 2)
-    k_schur(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
-            const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
-            const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
-            const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ Vptr,
-            const int32_t* __restrict__ Vcol, const double* __restrict__ Vval, double tau,
-            int32_t* __restrict__ scratch_all, int64_t* __restrict__ row_cnt, int64_t* __restrict__ row_off,
-            int32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, int64_t cap,
-            unsigned long long* __restrict__ cursor, int64_t* __restrict__ lrow_cnt, int64_t* __restrict__ lrow_off,
-            int32_t* __restrict__ ltmp_col, double* __restrict__ ltmp_val, int64_t lcap,
-            unsigned long long* __restrict__ lcursor, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
-            int* __restrict__ error) {
-  constexpr int T = GLOBAL ? HTG : HT;
-  constexpr int BM = GLOBAL ? BMAXG : BMAX;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int scount[SW], sbcount[SW];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* wscr = scratch_all + (size_t)(blockIdx.x * SW + wid) * schur_scratch_words<T, GLOBAL>();
-  int32_t* list = wscr;                                         // T int32
-  double* kvals = reinterpret_cast<double*>(wscr + T);          // T doubles
-  double* vals;
-  int32_t* tab;
-  BlkEnt* blk;
-  int32_t* bperm;  // blocks in ascending key order (indices into blk)
-  if constexpr (GLOBAL) {
-    tab = wscr + 3 * T;                                         // T int32
-    vals = reinterpret_cast<double*>(wscr + 4 * T);             // T doubles
-    blk = reinterpret_cast<BlkEnt*>(wscr + 6 * T);
-    bperm = wscr + 6 * T + (size_t)BM * (sizeof(BlkEnt) / 4);
-  } else {
-    vals = reinterpret_cast<double*>(smem_raw) + (size_t)wid * T;
-    tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)SW * T * sizeof(double)) + (size_t)wid * T;
-    blk = reinterpret_cast<BlkEnt*>(wscr + 3 * T);
-    bperm = wscr + 3 * T + (size_t)BM * (sizeof(BlkEnt) / 4);
-  }
-  for (int t = lane; t < T; t += 32) tab[t] = -1;  // reset incrementally after each row
-  __syncwarp();
-  for (int ri = blockIdx.x * SW + wid; ri < nrows; ri += gridDim.x * SW) {
-    const int cp = rowlist ? rowlist[ri] : ri;
-    const int c = cidx[cp];
-    const int64_t lo = ptr[c], hi = ptr[c + 1];
-    __syncwarp();
-    if (lane == 0) {
-      scount[wid] = 0;
-      sbcount[wid] = 0;
-    }
-    __syncwarp();
-    bool full = false;
-    // (1a) the F blocks adjacent to row c: real blocks (1x1 / 2x2 pivots) and the
-    //      virtual blocks of the couplings of adjacent pivot singles (reading R17)
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-      const int32_t u = col[e];
-      if (!inF[u]) continue;
-      const int32_t p = partner[u];
-      bool take = true;
-      double a_cp = 0.0;
-      if (p >= 0) {
-        const int64_t ep = lookup_idx(col, lo, hi, p);
-        if (ep >= 0) a_cp = ah[ep];
-        if (ep >= 0 && p < u) take = false;
-      }
-      if (take) {
-        const int bpos = atomicAdd(&sbcount[wid], 1);
-        if (bpos < BM) {
-          BlkEnt bb;
-          if (p < 0) {
-            bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
-            bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
-          } else {
-            bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
-            bb.acf = (bb.f == u) ? ah[e] : a_cp;
-            bb.acg = (bb.g == u) ? ah[e] : a_cp;
-            bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
-          }
-          bb.key = ((int64_t)bb.lead << 32) | (int64_t)bb.lead;
-          blk[bpos] = bb;
-        }
-      }
-      if (p < 0 && Vptr) {
-        for (int64_t ev = Vptr[u]; ev < Vptr[u + 1]; ++ev) {
-          const int32_t v = Vcol[ev];
-          const int64_t evc = lookup_idx(col, lo, hi, v);
-          if (evc >= 0 && v < u) continue;  // taken at the smaller adjacent member
-          const int bpos = atomicAdd(&sbcount[wid], 1);
-          if (bpos < BM) {
-            BlkEnt bb;
-            bb.f = min(u, v); bb.g = max(u, v); bb.lead = bb.f;
-            const double a_cv = (evc >= 0) ? ah[evc] : 0.0;
-            bb.acf = (bb.f == u) ? ah[e] : a_cv;
-            bb.acg = (bb.g == u) ? ah[e] : a_cv;
-            bb.Bff = 0.0; bb.Bgg = 0.0; bb.Bfg = Vval[ev];
-            bb.key = ((int64_t)bb.f << 32) | (int64_t)bb.g;
-            blk[bpos] = bb;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    const int nb = sbcount[wid];
-    // (1b) blocks in ascending key: bitonic sort of (key, index); keys in the free scratch
-    int64_t* skey = reinterpret_cast<int64_t*>(kvals);
-    int32_t* perm = list;
-    int PB = 1;
-    while (PB < nb) PB <<= 1;
-    if (nb <= BM) {
-      for (int t = lane; t < PB; t += 32) {
-        skey[t] = (t < nb) ? blk[t].key : INT64_MAX;
-        perm[t] = t;
-      }
-      __syncwarp();
-      for (int kk = 2; kk <= PB; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (int t = lane; t < PB; t += 32) {
-            const int ixj = t ^ jj;
-            if (ixj > t) {
-              const int64_t x = skey[t], y = skey[ixj];
-              const bool up = (t & kk) == 0;
-              if ((x > y) == up) {
-                skey[t] = y;
-                skey[ixj] = x;
-                const int32_t tp = perm[t];
-                perm[t] = perm[ixj];
-                perm[ixj] = tp;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-      for (int t = lane; t < nb; t += 32) bperm[t] = perm[t];
-      __syncwarp();
-    }
-    // (L) l_cx = sum over blocks (ascending key) of [(a_cf, a_cg) B_b]_x, from 0
-    int lkept = 0;
-    if (nb <= BM) {
-      if (lane == 0) {
-        for (int i = 0; i < nb; ++i) {
-          const BlkEnt& B = blk[bperm[i]];
-          if (B.g < 0) {
-            const int sl = hslot<T>(tab, vals, B.f, &scount[wid], list);
-            if (sl < 0) { full = true; break; }
-            vals[sl] = __dadd_rn(vals[sl], __dmul_rn(B.acf, B.Bff));
-          } else {
-            const int sf = hslot<T>(tab, vals, B.f, &scount[wid], list);
-            if (sf < 0) { full = true; break; }
-            vals[sf] = __dadd_rn(vals[sf], lval_pair(B.acf, B.acg, B.Bff, B.Bfg));
-            const int sg = hslot<T>(tab, vals, B.g, &scount[wid], list);
-            if (sg < 0) { full = true; break; }
-            vals[sg] = __dadd_rn(vals[sg], lval_pair(B.acf, B.acg, B.Bfg, B.Bgg));
-          }
-        }
-      }
-      __syncwarp();
-      // drop the L row, compact the survivors behind the block keys (skey[PB..]) and
-      // their columns (list[2*PB + ...], trailing the slot reads), reset the slots
-      const int nl = min(scount[wid], T);
-      double* lv_out = kvals;
-      int32_t* lc_out = list;
-      for (int t0 = 0; t0 < nl; t0 += 32) {
-        const int t = t0 + lane;
-        bool keep = false;
-        int32_t kk = 0;
-        double vv = 0.0;
-        if (t < nl) {
-          const int32_t sl = lc_out[t];
-          kk = tab[sl];
-          vv = vals[sl];
-          tab[sl] = -1;
-          keep = fabs(vv) >= tau;
-        }
-        __syncwarp();
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-          const int off = lkept + __popc(bal & ((1u << lane) - 1u));
-          lc_out[off] = kk;
-          lv_out[off] = vv;
-        }
-        lkept += __popc(bal);
-        __syncwarp();
-      }
-      if (!__any_sync(0xffffffffu, full)) {
-        unsigned long long lb = 0;
-        if (lane == 0) lb = atomicAdd(lcursor, (unsigned long long)lkept);
-        lb = __shfl_sync(0xffffffffu, lb, 0);
-        if (lane == 0) {
-          lrow_cnt[cp] = lkept;
-          lrow_off[cp] = (int64_t)lb;
-        }
-        if ((int64_t)lb + lkept <= lcap)
-          for (int t = lane; t < lkept; t += 32) {
-            ltmp_col[lb + t] = lc_out[t];
-            ltmp_val[lb + t] = lv_out[t];
-          }
-      }
-      __syncwarp();
-      if (lane == 0) scount[wid] = 0;
-      __syncwarp();
-    }
-    // (1c) s_cc' = a^_cc' for the coarse neighbours of c
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-      const int32_t cu = cmap[col[e]];  // -1 on pivots
-      if (cu < 0) continue;
-      const int sl = hslot<T>(tab, vals, cu, &scount[wid], list);
-      if (sl < 0)
-        full = true;
-      else
-        vals[sl] = ah[e];
-    }
-    __syncwarp();
-    // (2) subtract the block terms: the real blocks in ascending key (they and A^_CC
-    //     define the pattern of the row), then the virtual blocks in ascending key,
-    //     restricted to that pattern -- no fill from the compensation (reading R17).
-    //     Each lane gathers SU entries of a block row before hashing them (ILP).
-    if (nb <= BM) {
-      constexpr int SU = 4;
-      for (int vpass = 0; vpass < 2; ++vpass) {
-        for (int bi = 0; bi < nb && !__any_sync(0xffffffffu, full); ++bi) {
-          const BlkEnt B = blk[bperm[bi]];
-          const bool virt = (int32_t)(B.key >> 32) != (int32_t)(B.key & 0xffffffffLL);
-          if (virt != (vpass == 1)) continue;
-          if (B.g < 0) {
-            const int64_t r0 = ptr[B.f], r1 = ptr[B.f + 1];
-            for (int64_t e0 = r0 + lane; e0 < r1; e0 += 32 * SU) {
-              int32_t cv[SU];
-              double av[SU];
-#pragma unroll
-              for (int u = 0; u < SU; ++u) {
-                const int64_t e = e0 + 32 * u;
-                cv[u] = (e < r1) ? col[e] : -1;
-                av[u] = (e < r1) ? ah[e] : 0.0;
-              }
-#pragma unroll
-              for (int u = 0; u < SU; ++u) cv[u] = (cv[u] >= 0) ? cmap[cv[u]] : -1;
-#pragma unroll
-              for (int u = 0; u < SU; ++u) {
-                if (cv[u] < 0) continue;
-                const int sl = hslot<T>(tab, vals, cv[u], &scount[wid], list);
-                if (sl < 0) {
-                  full = true;
-                  continue;
-                }
-                vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, av[u])));
-              }
-            }
-          } else {
-            // rows f and g: entries of f (with a_{c'g} looked up in g), then entries only
-            // in g.  A virtual block's term B_fg (a_cf a_c'g + a_cg a_c'f) vanishes on the
-            // row whose weight (a_cg for row f, a_cf for row g) is 0: that row is skipped.
-            const bool walk_f = !virt || B.acg != 0.0, walk_g = !virt || B.acf != 0.0;
-            const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
-            const int64_t nf = walk_f ? f1 - f0 : 0, ntot = nf + (walk_g ? g1 - g0 : 0);
-            for (int64_t q0 = lane; q0 < ntot; q0 += 32 * SU) {
-              int32_t vv[SU], cv[SU];
-              double av[SU];
-#pragma unroll
-              for (int u = 0; u < SU; ++u) {
-                const int64_t q = q0 + 32 * u;
-                const int64_t e = (q < nf) ? f0 + q : g0 + (q - nf);
-                vv[u] = (q < ntot) ? col[e] : -1;
-                av[u] = (q < ntot) ? ah[e] : 0.0;
-              }
-#pragma unroll
-              for (int u = 0; u < SU; ++u) cv[u] = (vv[u] >= 0) ? cmap[vv[u]] : -1;
-#pragma unroll
-              for (int u = 0; u < SU; ++u) {
-                if (cv[u] < 0) continue;
-                const bool pass = (q0 + 32 * u) >= nf;
-                double a2f, a2g;
-                if (!pass) {
-                  a2f = av[u];
-                  const int64_t eg = walk_g ? lookup_idx(col, g0, g1, vv[u]) : -1;
-                  a2g = (eg >= 0) ? ah[eg] : 0.0;
-                } else {
-                  if (walk_f && lookup_idx(col, f0, f1, vv[u]) >= 0) continue;  // handled with row f
-                  a2f = 0.0;
-                  a2g = av[u];
-                }
-                int sl;
-                if (virt) {
-                  sl = hfind<T>(tab, cv[u]);
-                  if (sl < 0) continue;  // outside the pattern
-                } else {
-                  sl = hslot<T>(tab, vals, cv[u], &scount[wid], list);
-                  if (sl < 0) {
-                    full = true;
-                    continue;
-                  }
-                }
-                const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
-                                            __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
-                const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
-                vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-    }
-    const int nc = min(scount[wid], T);
-    const bool bad = (nb > BM) || __any_sync(0xffffffffu, full) || scount[wid] > (T * 3) / 4;
-    // (3) collect (key, value) through the slot list, reset the slots, drop, and
-    //     compact the survivors (only those are sorted)
-    int32_t* keys = list;  // aliases the slot list: writes trail the reads
-    int kept = 0;
-    for (int t0 = 0; t0 < nc; t0 += 32) {
-      const int t = t0 + lane;
-      bool keep = false;
-      int32_t kk = 0;
-      double vv = 0.0;
-      if (t < nc) {
-        const int32_t sl = list[t];
-        kk = tab[sl];
-        vv = vals[sl];
-        tab[sl] = -1;
-        keep = (kk == cp) || (fabs(vv) >= tau);
-      }
-      __syncwarp();
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int off = kept + __popc(bal & ((1u << lane) - 1u));
-        keys[off] = kk;
-        kvals[off] = vv;
-      }
-      kept += __popc(bal);
-      __syncwarp();
-    }
-    if (bad) {
-      if (GLOBAL) {
-        if (lane == 0) atomicExch(error, nb > BM ? 1 : 2);
-      } else if (lane == 0) {
-        ovf_list[atomicAdd(ovf_count, 1)] = cp;
-      }
-      continue;
-    }
-    int P = 1;
-    while (P < kept) P <<= 1;
-    for (int t = lane; t < P; t += 32) {  // sort the survivors in the (now empty) table storage
-      tab[t] = (t < kept) ? keys[t] : INT32_MAX;
-      vals[t] = (t < kept) ? kvals[t] : 0.0;
-    }
-    __syncwarp();
-    warp_bitonic_sort_kv(tab, vals, P);
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)kept);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (lane == 0) {
-      row_cnt[cp] = kept;
-      row_off[cp] = (int64_t)base;
-    }
-    if ((int64_t)base + kept <= cap) {
-      for (int t = lane; t < kept; t += 32) {
-        tmp_col[base + t] = tab[t];
-        tmp_val[base + t] = vals[t];
-      }
-    }
-    __syncwarp();
-    for (int t = lane; t < P; t += 32) tab[t] = -1;  // the table is empty again
-    __syncwarp();
-  }
-}
-
-// CTA-per-row variant of k_schur for the rows the warp variant cannot hold (more
-// than 3/4 HT candidates): the same arithmetic in the same per-entry order, one
-// CTA of CT threads per row, the table (HTC entries) in shared memory.  The block
-// terms are applied block after block with a barrier in between; each coarse
-// neighbour c' appears at most once per block, so threads never share a slot
-// inside a block.  Rows that still do not fit are queued to ovf_list.
-constexpr int CT = 256;
-constexpr int HTC_A = 8192;    // tier 2a: 96 KB of shared memory, two CTAs (rows) per SM
-constexpr int HTC_B = 16384;   // tier 2b: 192 KB, one CTA per SM
-constexpr int BMAXC = 2048;
-template <int HT2>
-constexpr size_t schur_cta_smem() { return (size_t)HT2 * (sizeof(int32_t) + sizeof(double)); }
-template <int HT2>
-constexpr size_t schur_cta_scratch_words() { return (size_t)HT2 * 4 + (size_t)BMAXC * (sizeof(BlkEnt) / 4 + 1); }
-
-__device__ __forceinline__ void cta_bitonic_sort_kv(int32_t* a, double* v, int P) {
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < P; t += CT) {
-        const int ixj = t ^ j;
-        if (ixj > t) {
-          const int32_t x = a[t], y = a[ixj];
-          const bool up = (t & k) == 0;
-          if ((x > y) == up) {
-            a[t] = y;
-            a[ixj] = x;
-            const double tv = v[t];
-            v[t] = v[ixj];
-            v[ixj] = tv;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-template <int HTC>
-__global__ void __launch_bounds__(CT, HTC <= 8192 ? 2 : 1)
-    k_schur_cta(int nrows, const int32_t* __restrict__ rowlist, const int32_t* __restrict__ cidx,
-                const int32_t* __restrict__ cmap, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                const double* __restrict__ ah, const int8_t* __restrict__ inF, const int32_t* __restrict__ partner,
-                const double* __restrict__ b11, const double* __restrict__ b12, const int64_t* __restrict__ Vptr,
-                const int32_t* __restrict__ Vcol, const double* __restrict__ Vval, double tau,
-                int32_t* __restrict__ scratch_all, int64_t* __restrict__ row_cnt, int64_t* __restrict__ row_off,
-                int32_t* __restrict__ tmp_col, double* __restrict__ tmp_val, int64_t cap,
-                unsigned long long* __restrict__ cursor, int64_t* __restrict__ lrow_cnt,
-                int64_t* __restrict__ lrow_off, int32_t* __restrict__ ltmp_col, double* __restrict__ ltmp_val,
-                int64_t lcap, unsigned long long* __restrict__ lcursor, int32_t* __restrict__ ovf_list,
-                int* __restrict__ ovf_count) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int scount, sbcount, sfull, skept;
-  __shared__ unsigned long long sbase;
-  double* vals = reinterpret_cast<double*>(smem_raw);
-  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw + (size_t)HTC * sizeof(double));
-  const int tid = threadIdx.x, lane = tid & 31;
-  int32_t* wscr = scratch_all + (size_t)blockIdx.x * schur_cta_scratch_words<HTC>();
-  int32_t* list = wscr;                                          // HTC int32 (slot list)
-  double* kvals = reinterpret_cast<double*>(wscr + HTC);         // HTC doubles
-  int32_t* keys2 = wscr + 3 * HTC;                               // HTC int32
-  BlkEnt* blk = reinterpret_cast<BlkEnt*>(wscr + 4 * HTC);
-  int32_t* bperm = wscr + 4 * HTC + (size_t)BMAXC * (sizeof(BlkEnt) / 4);
-  for (int t = tid; t < HTC; t += CT) tab[t] = -1;
-  __syncthreads();
-  for (int ri = blockIdx.x; ri < nrows; ri += gridDim.x) {
-    const int cp = rowlist[ri];
-    const int c = cidx[cp];
-    const int64_t lo = ptr[c], hi = ptr[c + 1];
-    if (tid == 0) {
-      scount = 0;
-      sbcount = 0;
-      sfull = 0;
-      skept = 0;
-    }
-    __syncthreads();
-    // (1a) real and virtual blocks adjacent to row c (as in k_schur)
-    for (int64_t e = lo + tid; e < hi; e += CT) {
-      const int32_t u = col[e];
-      if (!inF[u]) continue;
-      const int32_t p = partner[u];
-      bool take = true;
-      double a_cp = 0.0;
-      if (p >= 0) {
-        const int64_t ep = lookup_idx(col, lo, hi, p);
-        if (ep >= 0) a_cp = ah[ep];
-        if (ep >= 0 && p < u) take = false;
-      }
-      if (take) {
-        const int bpos = atomicAdd(&sbcount, 1);
-        if (bpos < BMAXC) {
-          BlkEnt bb;
-          if (p < 0) {
-            bb.f = u; bb.g = -1; bb.lead = u; bb.acf = ah[e]; bb.acg = 0.0;
-            bb.Bff = b11[u]; bb.Bgg = 0.0; bb.Bfg = 0.0;
-          } else {
-            bb.f = min(u, p); bb.g = max(u, p); bb.lead = bb.f;
-            bb.acf = (bb.f == u) ? ah[e] : a_cp;
-            bb.acg = (bb.g == u) ? ah[e] : a_cp;
-            bb.Bff = b11[bb.f]; bb.Bgg = b11[bb.g]; bb.Bfg = b12[bb.f];
-          }
-          bb.key = ((int64_t)bb.lead << 32) | (int64_t)bb.lead;
-          blk[bpos] = bb;
-        }
-      }
-      if (p < 0 && Vptr) {
-        for (int64_t ev = Vptr[u]; ev < Vptr[u + 1]; ++ev) {
-          const int32_t v = Vcol[ev];
-          const int64_t evc = lookup_idx(col, lo, hi, v);
-          if (evc >= 0 && v < u) continue;
-          const int bpos = atomicAdd(&sbcount, 1);
-          if (bpos < BMAXC) {
-            BlkEnt bb;
-            bb.f = min(u, v); bb.g = max(u, v); bb.lead = bb.f;
-            const double a_cv = (evc >= 0) ? ah[evc] : 0.0;
-            bb.acf = (bb.f == u) ? ah[e] : a_cv;
-            bb.acg = (bb.g == u) ? ah[e] : a_cv;
-            bb.Bff = 0.0; bb.Bgg = 0.0; bb.Bfg = Vval[ev];
-            bb.key = ((int64_t)bb.f << 32) | (int64_t)bb.g;
-            blk[bpos] = bb;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    const int nb = sbcount;
-    bool bad = nb > BMAXC;
-    if (!bad) {
-      // (1b) ascending block key
-      int64_t* skey = reinterpret_cast<int64_t*>(kvals);
-      int32_t* perm = list;
-      int PB = 1;
-      while (PB < nb) PB <<= 1;
-      for (int t = tid; t < PB; t += CT) {
-        skey[t] = (t < nb) ? blk[t].key : INT64_MAX;
-        perm[t] = t;
-      }
-      __syncthreads();
-      for (int kk = 2; kk <= PB; kk <<= 1) {
-        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (int t = tid; t < PB; t += CT) {
-            const int ixj = t ^ jj;
-            if (ixj > t) {
-              const int64_t x = skey[t], y = skey[ixj];
-              const bool up = (t & kk) == 0;
-              if ((x > y) == up) {
-                skey[t] = y;
-                skey[ixj] = x;
-                const int32_t tp = perm[t];
-                perm[t] = perm[ixj];
-                perm[ixj] = tp;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-      for (int t = tid; t < nb; t += CT) bperm[t] = perm[t];
-      __syncthreads();
-      // (L) sequential accumulation in ascending key (thread 0), then warp 0 drops,
-      //     compacts and emits the row of L
-      if (tid == 0) {
-        for (int i = 0; i < nb; ++i) {
-          const BlkEnt& B = blk[bperm[i]];
-          if (B.g < 0) {
-            const int sl = hslot<HTC>(tab, vals, B.f, &scount, list);
-            if (sl < 0) { sfull = 1; break; }
-            vals[sl] = __dadd_rn(vals[sl], __dmul_rn(B.acf, B.Bff));
-          } else {
-            const int sf = hslot<HTC>(tab, vals, B.f, &scount, list);
-            if (sf < 0) { sfull = 1; break; }
-            vals[sf] = __dadd_rn(vals[sf], lval_pair(B.acf, B.acg, B.Bff, B.Bfg));
-            const int sg = hslot<HTC>(tab, vals, B.g, &scount, list);
-            if (sg < 0) { sfull = 1; break; }
-            vals[sg] = __dadd_rn(vals[sg], lval_pair(B.acf, B.acg, B.Bfg, B.Bgg));
-          }
-        }
-      }
-      __syncthreads();
-      if (tid < 32) {
-        const int nl = min(scount, HTC);
-        int lkept = 0;
-        for (int t0 = 0; t0 < nl; t0 += 32) {
-          const int t = t0 + lane;
-          bool keep = false;
-          int32_t kk = 0;
-          double vv = 0.0;
-          if (t < nl) {
-            const int32_t sl = list[t];
-            kk = tab[sl];
-            vv = vals[sl];
-            tab[sl] = -1;
-            keep = fabs(vv) >= tau;
-          }
-          __syncwarp();
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) {
-            const int off = lkept + __popc(bal & ((1u << lane) - 1u));
-            list[off] = kk;
-            kvals[off] = vv;
-          }
-          lkept += __popc(bal);
-          __syncwarp();
-        }
-        if (!sfull) {
-          unsigned long long lb = 0;
-          if (lane == 0) lb = atomicAdd(lcursor, (unsigned long long)lkept);
-          lb = __shfl_sync(0xffffffffu, lb, 0);
-          if (lane == 0) {
-            lrow_cnt[cp] = lkept;
-            lrow_off[cp] = (int64_t)lb;
-          }
-          if ((int64_t)lb + lkept <= lcap)
-            for (int t = lane; t < lkept; t += 32) {
-              ltmp_col[lb + t] = list[t];
-              ltmp_val[lb + t] = kvals[t];
-            }
-        }
-        if (lane == 0) scount = 0;
-      }
-      __syncthreads();
-    }
-    // (1c) s_cc' = a^_cc'
-    for (int64_t e = lo + tid; e < hi; e += CT) {
-      const int32_t cu = cmap[col[e]];
-      if (cu < 0) continue;
-      const int sl = hslot<HTC>(tab, vals, cu, &scount, list);
-      if (sl < 0)
-        sfull = 1;
-      else
-        vals[sl] = ah[e];
-    }
-    __syncthreads();
-    // (2) real blocks, then virtual blocks on the pattern (as in k_schur)
-    bool full_any = sfull != 0;  // uniform: read after the barrier; sfull is not written below
-    if (!bad && !full_any) {
-      bool lfull = false;
-      for (int vpass = 0; vpass < 2 && !full_any; ++vpass) {
-        for (int bi = 0; bi < nb; ++bi) {
-          const BlkEnt B = blk[bperm[bi]];
-          const bool virt = (int32_t)(B.key >> 32) != (int32_t)(B.key & 0xffffffffLL);
-          if (virt != (vpass == 1)) continue;
-          if (B.g < 0) {
-            for (int64_t e = ptr[B.f] + tid; e < ptr[B.f + 1]; e += CT) {
-              const int32_t cv = cmap[col[e]];
-              if (cv < 0) continue;
-              const int sl = hslot<HTC>(tab, vals, cv, &scount, list);
-              if (sl < 0) {
-                lfull = true;
-                continue;
-              }
-              vals[sl] = __dsub_rn(vals[sl], __dmul_rn(B.Bff, __dmul_rn(B.acf, ah[e])));
-            }
-          } else {
-            const bool walk_f = !virt || B.acg != 0.0, walk_g = !virt || B.acf != 0.0;
-            const int64_t f0 = ptr[B.f], f1 = ptr[B.f + 1], g0 = ptr[B.g], g1 = ptr[B.g + 1];
-            const int64_t nf = walk_f ? f1 - f0 : 0, ng = walk_g ? g1 - g0 : 0;
-            for (int64_t q = tid; q < nf + ng; q += CT) {
-              const bool pass = q >= nf;
-              const int64_t e = pass ? g0 + (q - nf) : f0 + q;
-              const int32_t v = col[e];
-              const int32_t cv = cmap[v];
-              if (cv < 0) continue;
-              double a2f, a2g;
-              if (!pass) {
-                a2f = ah[e];
-                const int64_t eg = walk_g ? lookup_idx(col, g0, g1, v) : -1;
-                a2g = (eg >= 0) ? ah[eg] : 0.0;
-              } else {
-                if (walk_f && lookup_idx(col, f0, f1, v) >= 0) continue;
-                a2f = 0.0;
-                a2g = ah[e];
-              }
-              int sl;
-              if (virt) {
-                sl = hfind<HTC>(tab, cv);
-                if (sl < 0) continue;
-              } else {
-                sl = hslot<HTC>(tab, vals, cv, &scount, list);
-                if (sl < 0) {
-                  lfull = true;
-                  continue;
-                }
-              }
-              const double t1 = __dadd_rn(__dmul_rn(B.Bff, __dmul_rn(B.acf, a2f)),
-                                          __dmul_rn(B.Bgg, __dmul_rn(B.acg, a2g)));
-              const double t2 = __dmul_rn(B.Bfg, __dadd_rn(__dmul_rn(B.acf, a2g), __dmul_rn(B.acg, a2f)));
-              vals[sl] = __dsub_rn(vals[sl], __dadd_rn(t1, t2));
-            }
-          }
-          if (__syncthreads_or(lfull)) {
-            full_any = true;
-            break;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    const int nc = min(scount, HTC);
-    bad = bad || full_any || scount > (HTC * 3) / 4;
-    // (3) collect through the slot list, reset the slots, drop; survivors in any order
-    for (int t = tid; t < nc; t += CT) {
-      const int32_t sl = list[t];
-      const int32_t kk = tab[sl];
-      const double vv = vals[sl];
-      tab[sl] = -1;
-      if (!bad && ((kk == cp) || (fabs(vv) >= tau))) {
-        const int off = atomicAdd(&skept, 1);
-        keys2[off] = kk;
-        kvals[off] = vv;
-      }
-    }
-    __syncthreads();
-    if (bad) {
-      if (tid == 0) ovf_list[atomicAdd(ovf_count, 1)] = cp;
-      continue;  // uniform
-    }
-    const int kept = skept;
-    int P = 1;
-    while (P < kept) P <<= 1;
-    for (int t = tid; t < P; t += CT) {
-      tab[t] = (t < kept) ? keys2[t] : INT32_MAX;
-      vals[t] = (t < kept) ? kvals[t] : 0.0;
-    }
-    __syncthreads();
-    cta_bitonic_sort_kv(tab, vals, P);
-    if (tid == 0) {
-      sbase = atomicAdd(cursor, (unsigned long long)kept);
-      row_cnt[cp] = kept;
-      row_off[cp] = (int64_t)sbase;
-    }
-    __syncthreads();
-    const unsigned long long base = sbase;
-    if ((int64_t)base + kept <= cap)
-      for (int t = tid; t < kept; t += CT) {
-        tmp_col[base + t] = tab[t];
-        tmp_val[base + t] = vals[t];
-      }
-    __syncthreads();
-    for (int t = tid; t < P; t += CT) tab[t] = -1;
-    __syncthreads();
-  }
-}
-
-// gather the per-row runs of the one-pass Schur output into CSR order
-__global__ void k_schur_gather(int nC, const int64_t* __restrict__ Sptr, const int64_t* __restrict__ row_off,
-                               const int32_t* __restrict__ tmp_col, const double* __restrict__ tmp_val,
-                               int32_t* __restrict__ Scol, double* __restrict__ Sval) {
-  const int lane = threadIdx.x & 31;
-  for (int cp = (blockIdx.x * TB + threadIdx.x) >> 5; cp < nC; cp += (gridDim.x * TB) >> 5) {
-    const int64_t d0 = Sptr[cp], cnt = Sptr[cp + 1] - d0, s0 = row_off[cp];
-    for (int64_t t = lane; t < cnt; t += 32) {
-      Scol[d0 + t] = tmp_col[s0 + t];
-      Sval[d0 + t] = tmp_val[s0 + t];
-    }
-  }
 }
 
 // ----------------------------------------------------------------------------
@@ -1885,7 +1048,7 @@ void Level::release(cudaStream_t st) {
 
 // Factor one level.  Returns false on stall (nothing allocated into lv then).
 static bool verbose_setup();
-static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P, Level& lv, Csr& S,
+static bool factor_level(const Csr& A, int latticeL, int z0, const aj_precond_params& P, Level& lv, Csr& S,
                          cudaStream_t st) {
   const int n = A.n;
   const int g = grid_for(n);
@@ -1919,7 +1082,7 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
                               counters + 0);
     AJ_LAUNCHED();
   }
-  k_blocks<<<g, TB, 0, st>>>(n, latticeL, ok1, dg, lmax1, partner, leader, q, b11, inF);
+  k_blocks<<<g, TB, 0, st>>>(n, latticeL, z0, ok1, dg, lmax1, partner, leader, q, b11, inF);
   AJ_LAUNCHED();
 
   int rounds = 0;
@@ -2040,128 +1203,48 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
     }
     dfree(cnt, st);
   }
-  // L rows and the Schur complement on the coarse nodes, one pass: the survivors of
+  // L rows and the Schur complement on the coarse nodes (aj_schur.cu): the survivors of
   // each row are appended to temp buffers through global cursors, then gathered
   {
     S.n = nC;
-    const int nwarps_total = std::min(std::max(nC, 1), num_sms() * 8 * SW);
-    const int gs = std::max(1, ceil_div(nwarps_total, SW));
-    const int gsg2 = std::min(gs, num_sms());  // fallback grids (large tables)
-    int32_t* scr = dalloc<int32_t>((size_t)gs * SW * schur_scratch_words<HT, false>(), st);
-    int64_t* row_cnt = dalloc<int64_t>(std::max(nC, 1), st);
-    int64_t* row_off = dalloc<int64_t>(std::max(nC, 1), st);
-    int64_t* lrow_cnt = dalloc<int64_t>(std::max(nC, 1), st);
-    int64_t* lrow_off = dalloc<int64_t>(std::max(nC, 1), st);
-    int32_t* ovf_list = dalloc<int32_t>(std::max(nC, 1), st);
-    unsigned long long* cursor = dalloc<unsigned long long>(2, st);
-    int* ovf = counters + 5;   // [5] fallback rows, [6] error
-    {  // per level (cheap): the limit is a per-device property of the function, and the
-       // calling thread may drive a different device than on the previous setup
-      AJ_CUDA(cudaFuncSetAttribute(k_schur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
-      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)schur_cta_smem<HTC_A>()));
-      AJ_CUDA(cudaFuncSetAttribute(k_schur_cta<HTC_B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)schur_cta_smem<HTC_B>()));
-    }
-    int32_t* ovf2_list = nullptr;
-    int32_t* ovf3_list = nullptr;
-    int32_t* scrc = nullptr;
-    int64_t cap = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
-    int64_t lcap = std::max<int64_t>((int64_t)nC * 64, 1024);
-    int nov = 0;
-    int32_t *tmp_col = nullptr, *ltmp_col = nullptr;
-    double *tmp_val = nullptr, *ltmp_val = nullptr;
-    int32_t* scrg = nullptr;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      tmp_col = dalloc<int32_t>(cap, st);
-      tmp_val = dalloc<double>(cap, st);
-      ltmp_col = dalloc<int32_t>(lcap, st);
-      ltmp_val = dalloc<double>(lcap, st);
-      AJ_CUDA(cudaMemsetAsync(ovf, 0, 3 * sizeof(int), st));
-      AJ_CUDA(cudaMemsetAsync(cursor, 0, 2 * sizeof(unsigned long long), st));
-      // AJ_SCHUR_TIER=2/3 (testing): start every row at the CTA / global-table variant
-      const char* ftier = getenv("AJ_SCHUR_TIER");
-      const int first_tier = ftier ? atoi(ftier) : 1;
-      if (first_tier <= 1) {
-        k_schur<false><<<gs, SW * 32, kSchurSmem, st>>>(nC, nullptr, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF,
-                                                         partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scr,
-                                                         row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt,
-                                                         lrow_off, ltmp_col, ltmp_val, lcap, cursor + 1, ovf_list, ovf,
-                                                         ovf + 1);
-        AJ_LAUNCHED();
-        nov = read_scalar(ovf, st);
-      } else {
-        nov = nC;
-        k_iota<<<g, TB, 0, st>>>(nC, ovf_list);
-        AJ_LAUNCHED();
-      }
-      // AJ_SCHUR_TIER (testing): 2 = start at tier 2a, 4 = at tier 2b, 3 = at tier 3
-      int nov2 = 0;
-      if (nov > 0 && first_tier == 3) {
-        nov2 = nov;
-        if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
-        k_iota<<<g, TB, 0, st>>>(nC, ovf2_list);
-        AJ_LAUNCHED();
-      } else if (nov > 0) {
-        if (!scrc) scrc = dalloc<int32_t>((size_t)2 * gsg2 * schur_cta_scratch_words<HTC_B>(), st);
-        if (!ovf2_list) ovf2_list = dalloc<int32_t>(std::max(nov, 1), st);
-        if (!ovf3_list) ovf3_list = dalloc<int32_t>(std::max(nov, 1), st);
-        const int32_t* in_list = ovf_list;
-        int nin = nov;
-        if (first_tier != 4) {
-          // tier 2a: one CTA per row, 8192-entry shared-memory table, two rows per SM
-          AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
-          k_schur_cta<HTC_A><<<std::min(nov, 2 * gsg2), CT, schur_cta_smem<HTC_A>(), st>>>(
-              nov, ovf_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
-              P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
-              ltmp_val, lcap, cursor + 1, ovf3_list, ovf + 2);
-          AJ_LAUNCHED();
-          nin = read_scalar(ovf + 2, st);
-          in_list = ovf3_list;
-        }
-        if (nin > 0) {
-          // tier 2b: one CTA per row, 16384-entry shared-memory table
-          AJ_CUDA(cudaMemsetAsync(ovf + 2, 0, sizeof(int), st));
-          k_schur_cta<HTC_B><<<std::min(nin, gsg2), CT, schur_cta_smem<HTC_B>(), st>>>(
-              nin, in_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11, b12, lv.Vptr, lv.Vcol, lv.Vval,
-              P.tau_drop, scrc, row_cnt, row_off, tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
-              ltmp_val, lcap, cursor + 1, ovf2_list, ovf + 2);
-          AJ_LAUNCHED();
-          nov2 = read_scalar(ovf + 2, st);
-        }
-      }
-      if (nov2 > 0) {
-        // tier 3: one warp per row, 32768-entry tables in global memory
-        if (!scrg) scrg = dalloc<int32_t>((size_t)gsg2 * SW * schur_scratch_words<HTG, true>(), st);
-        k_schur<true><<<gsg2, SW * 32, 0, st>>>(nov2, ovf2_list, lv.cidx, lv.cmap, A.ptr, A.col, ah, inF, partner, b11,
-                                                 b12, lv.Vptr, lv.Vcol, lv.Vval, P.tau_drop, scrg, row_cnt, row_off,
-                                                 tmp_col, tmp_val, cap, cursor, lrow_cnt, lrow_off, ltmp_col,
-                                                 ltmp_val, lcap, cursor + 1, ovf_list, ovf, ovf + 1);
-        AJ_LAUNCHED();
-        const int err = read_scalar(ovf + 1, st);
-        AJ_REQUIRE(err == 0, AJ_ERR_CAPACITY,
-                   err == 1 ? "Schur complement: more than 2048 pivot blocks adjacent to one row (raise tau_drop)"
-                            : "Schur complement: more than 24576 candidate columns in one row (raise tau_drop)");
-      }
-      unsigned long long used[2];
-      AJ_CUDA(cudaMemcpyAsync(used, cursor, sizeof(used), cudaMemcpyDeviceToHost, st));
-      AJ_CUDA(cudaStreamSynchronize(st));
-      if ((int64_t)used[0] <= cap && (int64_t)used[1] <= lcap) break;
-      for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val}) dfree(q, st);
-      cap = std::max<int64_t>(cap, (int64_t)used[0]);  // exact sizes now known: run again
-      lcap = std::max<int64_t>(lcap, (int64_t)used[1]);
-      AJ_REQUIRE(attempt == 0, AJ_ERR_CAPACITY, "Schur complement: temp capacity");
-      if (verbose_setup())
-        fprintf(stderr, "[aj setup] n=%d: Schur temp capacity retry (S %llu / %lld, L %llu / %lld)\n", n,
-                used[0], (long long)cap, used[1], (long long)lcap);
-    }
-    // S in CSR order
-    S.nnz = counts_to_ptr(row_cnt, S.ptr, nC, st);
-    S.col = dalloc<int32_t>(S.nnz, st);
-    S.val = dalloc<double>(S.nnz, st);
+    SchurIn si;
+    si.n = n;
+    si.nC = nC;
+    si.nF = nF;
+    si.ptr = A.ptr;
+    si.col = A.col;
+    si.ah = ah;
+    si.inF = inF;
+    si.partner = partner;
+    si.cmap = lv.cmap;
+    si.cidx = lv.cidx;
+    si.fmap = lv.fmap;
+    si.fidx = lv.fidx;
+    si.b11 = b11;
+    si.b12 = b12;
+    si.Vptr = lv.Vptr;
+    si.Vcol = lv.Vcol;
+    si.Vval = lv.Vval;
+    si.tau = P.tau_drop;
+    si.cap_hint = std::max<int64_t>(2 * A.nnz, (int64_t)nC * 16);
+    SchurOut so;
+    schur_level(si, so, st);
+    int64_t* row_cnt = so.row_cnt;
+    int64_t* row_off = so.row_off;
+    int64_t* lrow_cnt = so.lrow_cnt;
+    int64_t* lrow_off = so.lrow_off;
+    int32_t* tmp_col = so.tmp_col;
+    double* tmp_val = so.tmp_val;
+    int32_t* ltmp_col = so.ltmp_col;
+    double* ltmp_val = so.ltmp_val;
+    for (int t = 0; t < 6; ++t) lv.schur_tier_rows[t] = so.tier_rows[t];
+    lv.schur_ovf_rows = so.ovf_rows;
+    lv.nnzFC = so.nnz_fc;
+    lv.schur_products = so.products;
+    lv.nnzA = A.nnz;
+    // S in CSR order: the computed upper triangle and its mirror
+    schur_mirror(nC, so, S, st);
     const int gg = std::max(1, std::min(ceil_div((int64_t)nC * 32, TB), num_sms() * 32));
-    k_schur_gather<<<gg, TB, 0, st>>>(nC, S.ptr, row_off, tmp_col, tmp_val, S.col, S.val);
-    AJ_LAUNCHED();
     // L (forward rows over coarse nodes, values l*D_f) and L^T (rows over pivots, by sort)
     lv.nnzL = counts_to_ptr(lrow_cnt, lv.Lptr, nC, st);
     lv.nnzLT = lv.nnzL;
@@ -2202,18 +1285,9 @@ static bool factor_level(const Csr& A, int latticeL, const aj_precond_params& P,
       dfree(cntF, st);
     }
     for (void* q : {(void*)tkey, (void*)tkey2, (void*)traw, (void*)traw2}) dfree(q, st);
-    if (scrg) dfree(scrg, st);
-    if (scrc) dfree(scrc, st);
-    if (ovf2_list) dfree(ovf2_list, st);
-    if (ovf3_list) dfree(ovf3_list, st);
-    for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val, (void*)cursor, (void*)row_off,
-                    (void*)lrow_off, (void*)lrow_cnt})
+    for (void* q : {(void*)tmp_col, (void*)tmp_val, (void*)ltmp_col, (void*)ltmp_val, (void*)row_off, (void*)lrow_off,
+                    (void*)lrow_cnt, (void*)row_cnt})
       dfree(q, st);
-    lv.schur_fallback_rows = nov;
-    lv.schur_fallback_nb = nov > 0 ? read_scalar(ovf + 2, st) : 0;
-    dfree(scr, st);
-    dfree(ovf_list, st);
-    dfree(row_cnt, st);
     lv.nnzS = S.nnz;
   }
   dfree(partner, st);
@@ -2253,13 +1327,19 @@ aj_precond_params resolve_params(const aj_precond_params& in, int L) {
 
 Precond* precond_create(const double* eps, int L, double hop, double sigma, const aj_precond_params& Pin,
                         cudaStream_t st) {
+  return precond_create_slab(eps, L, 0, L, false, hop, sigma, Pin, st);
+}
+
+Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open_z, double hop, double sigma,
+                             const aj_precond_params& Pin, cudaStream_t st) {
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "precond_setup: L must be >= 3");
   const aj_precond_params P = resolve_params(Pin, L);
   (void)num_sms();  // device init: SM count + memory-pool release threshold
   AJ_REQUIRE(P.kappa > 1.0 && P.tau_drop >= 0.0 && P.tau_strong >= 0.0 && P.cand_cap >= 64,
              AJ_ERR_ARG, "precond_setup: invalid parameters");
-  const int64_t n64 = (int64_t)L * L * L;
-  AJ_REQUIRE(n64 < (int64_t)INT32_MAX, AJ_ERR_ARG, "precond_setup: L^3 exceeds int32 indexing");
+  AJ_REQUIRE(nz >= 1 && z0 >= 0 && z0 + nz <= L && (open_z || nz == L), AJ_ERR_ARG, "precond_setup: bad slab");
+  const int64_t n64 = (int64_t)L * L * nz;
+  AJ_REQUIRE(n64 < (int64_t)INT32_MAX, AJ_ERR_ARG, "precond_setup: L^2 nz exceeds int32 indexing");
   cudaEvent_t e0, e1;
   AJ_CUDA(cudaEventCreate(&e0));
   AJ_CUDA(cudaEventCreate(&e1));
@@ -2272,11 +1352,12 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   try {
     Csr A;
     A.n = (int)n64;
-    A.nnz = 7 * n64;
+    A.nnz = open_z ? (nz == 1 ? 5 * n64 : 7 * n64 - 2 * (int64_t)L * L) : 7 * n64;
+    K->nnzA0 = A.nnz;
     A.ptr = dalloc<int64_t>(n64 + 1, st);
     A.col = dalloc<int32_t>(A.nnz, st);
     A.val = dalloc<double>(A.nnz, st);
-    k_lattice_csr<<<std::min(grid_for(n64), num_sms() * 16), TB, 0, st>>>(L, eps, hop, sigma, A.ptr, A.col,
+    k_lattice_csr<<<std::min(grid_for(n64), num_sms() * 16), TB, 0, st>>>(L, nz, open_z ? 1 : 0, eps, hop, sigma, A.ptr, A.col,
                                                                            A.val);
     AJ_LAUNCHED();
     for (int lev = 0; lev < P.max_levels && lev < 1023; ++lev) {
@@ -2284,14 +1365,17 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
       Level lv;
       Csr S;
       const double t0 = verbose_setup() ? wall_ms() : 0.0;
-      if (!factor_level(A, lev == 0 ? L : 0, P, lv, S, st)) break;
+      if (!factor_level(A, lev == 0 ? L : 0, z0, P, lv, S, st)) break;
       if (verbose_setup()) {
         AJ_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr,
                 "[aj setup] level %d n=%d nF=%d pairs=%d virt=%lld mis_rounds=%d nnzA=%lld nnzS=%lld nnzL=%lld "
-                "fallback_rows=%d (tier3 %d) %.2f ms\n",
+                "nnzFC=%lld products=%lld tiers=%d/%d/%d/%d/%d/%d (C16->G %d) %.2f ms\n",
                 lev, lv.n, lv.nF, lv.npairs, (long long)lv.nnzV / 2, lv.rounds, (long long)A.nnz, (long long)S.nnz,
-                (long long)lv.nnzL, lv.schur_fallback_rows, lv.schur_fallback_nb, wall_ms() - t0);
+                (long long)lv.nnzL, (long long)lv.nnzFC, (long long)lv.schur_products, lv.schur_tier_rows[0],
+                lv.schur_tier_rows[1], lv.schur_tier_rows[2], lv.schur_tier_rows[3], lv.schur_tier_rows[4],
+                lv.schur_tier_rows[5], lv.schur_ovf_rows,
+                wall_ms() - t0);
       }
       if (lev > 0) {
         lv.r = dalloc<double>(lv.n, st);
@@ -2388,9 +1472,14 @@ Precond* precond_create(const double* eps, int L, double hop, double sigma, cons
   memset(&I, 0, sizeof(I));
   I.levels = (int)K->lv.size();
   I.coarse_n = K->nc;
-  I.nnz_A = 7 * n64;
+  I.nnz_A = K->nnzA0;
   for (size_t l = 0; l < K->lv.size(); ++l) {
     const Level& v = K->lv[l];
+    I.setup_products += v.schur_products;
+    // compulsory traffic of the level (12 B per (index, value) entry): read the level matrix,
+    // write and re-read its FC lists, stream one FC entry per Schur product, write S (temp
+    // run + CSR gather) and L (temp run, CSR, transpose)
+    I.setup_bytes += 12.0 * ((double)v.nnzA + 2.0 * v.nnzFC + (double)v.schur_products + 3.0 * v.nnzS + 4.0 * v.nnzL);
     I.nnz_L += v.nnzL;
     I.nnz_V += v.nnzV / 2;
     I.level_n[l] = v.n;

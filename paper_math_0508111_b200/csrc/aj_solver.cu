@@ -35,11 +35,25 @@ static int sgrid(int64_t n) {
 // scalar slots
 enum { S_TAU = 0, S_THETA, S_A1, S_A2, S_RX2, S_BRK, S_RHO0, S_RHO1, S_NB, S_COUNT = 16 };
 
+// the SQMR scalar recurrences of one step from ||r||^2 = rr, sigma_q = sig, alpha
+__device__ __forceinline__ void sqmr_B_scalars(double* sc, double rr, double sig, double alpha) {
+  const double tau = sc[S_TAU], th_old = sc[S_THETA];
+  const double th = sqrt(rr) / tau;
+  const double c2 = 1.0 / (1.0 + th * th);
+  sc[S_A1] = c2 * th_old * th_old;
+  sc[S_A2] = c2 * alpha;
+  sc[S_THETA] = th;
+  sc[S_TAU] = tau * th * sqrt(c2);
+  if (sig == 0.0 || !isfinite(alpha)) sc[S_BRK] = 1.0;
+}
+
 // t' = t - Qt c ;  alpha = rho/sigma_q ; r -= alpha t' ; ||r||^2 -> theta, tau, coefficients
+// (sharded: the last block leaves the local ||r||^2 in rb.out and k_sqmr_B_scalars runs
+// after the all-reduce)
 __global__ void __launch_bounds__(TB)
     k_sqmr_B(int64_t n, int m, const double* __restrict__ Qt, double* __restrict__ t, double* __restrict__ r,
              const double* __restrict__ dotsA, const double* __restrict__ rho_cur, double* __restrict__ sc,
-             RedBuf rb) {
+             RedBuf rb, int dist) {
   __shared__ double sc_c[32];
   if (threadIdx.x < m) sc_c[threadIdx.x] = dotsA[threadIdx.x];
   __syncthreads();
@@ -54,17 +68,13 @@ __global__ void __launch_bounds__(TB)
     r[s] = rv;
     acc[0] += rv * rv;
   }
-  if (block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x) && threadIdx.x == 0) {
-    const double rr = rb.out[0];
-    const double tau = sc[S_TAU], th_old = sc[S_THETA];
-    const double th = sqrt(rr) / tau;
-    const double c2 = 1.0 / (1.0 + th * th);
-    sc[S_A1] = c2 * th_old * th_old;
-    sc[S_A2] = c2 * alpha;
-    sc[S_THETA] = th;
-    sc[S_TAU] = tau * th * sqrt(c2);
-    if (sig == 0.0 || !isfinite(alpha)) sc[S_BRK] = 1.0;
-  }
+  if (block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x) && threadIdx.x == 0 && !dist)
+    sqmr_B_scalars(sc, rb.out[0], sig, alpha);
+}
+__global__ void k_sqmr_B_scalars(int m, const double* __restrict__ rr, const double* __restrict__ dotsA,
+                                 const double* __restrict__ rho_cur, double* __restrict__ sc) {
+  const double sig = dotsA[m];
+  sqmr_B_scalars(sc, rr[0], sig, (*rho_cur) / sig);
 }
 
 // d = a1 d + a2 q ; x += d ; s = a1 s + a2 t' ; rx -= s ; ||rx||^2
@@ -351,9 +361,10 @@ __global__ void k_resid(int64_t n, const double* __restrict__ Au, const double* 
   block_reduce_finalize<1, TB>(acc, rb, blockIdx.x, gridDim.x);
 }
 // start vector: uniform(-0.5, 0.5) from the counter stream `key`
-__global__ void k_start(int64_t n, uint64_t key, double* __restrict__ v) {
+// (s0: global index of the first local site, so a sharded start vector is the slice of the full one)
+__global__ void k_start(int64_t n, uint64_t key, double* __restrict__ v, int64_t s0) {
   for (int64_t s = blockIdx.x * (int64_t)TB + threadIdx.x; s < n; s += (int64_t)gridDim.x * TB)
-    v[s] = uniform01(key, (uint64_t)s) - 0.5;
+    v[s] = uniform01(key, (uint64_t)(s0 + s)) - 0.5;
 }
 // max |eps|
 __global__ void k_absmax(int64_t n, const double* __restrict__ x, unsigned long long* out) {
@@ -399,7 +410,7 @@ void Workspace::release(cudaStream_t st) {
 
 // SQMR on the projected operator.  Qt/Y: n x (m+1); column m of Qt holds q, column m of Y holds w.
 // b: right-hand side (already orthogonal to Q~); x: solution out.
-SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, double shift, const double* Qt,
+SqmrResult sqmr_run(const Precond* K, const double* eps, const Domain& dom, double hop, double shift, const double* Qt,
                     const double* Y, int m, const double* Hinv, const double* b, double* x, double tol,
                     int maxit, Workspace& ws, cudaStream_t st) {
   const int64_t n = ws.n;
@@ -421,6 +432,7 @@ SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, doub
   launch_fill(d, 0.0, n, st);
   launch_fill(sv, 0.0, n, st);
   launch_dot(nb2, b, b, n, ws.rs, st);
+  dom_allreduce(dom, nb2, 1, 0, st);
   k_sqmr_init_scalars<<<1, 1, 0, st>>>(sc, nb2);
   AJ_LAUNCHED();
   double hs[S_COUNT];
@@ -439,8 +451,12 @@ SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, doub
       precond_run(K, w, r, s2);
     else
       launch_copy(w, r, n, s2);
-    if (m > 0) launch_multi_dot(dQw, Qt, m, n, w, n, ws.rs, s2);
+    if (m > 0) {
+      launch_multi_dot(dQw, Qt, m, n, w, n, ws.rs, s2);
+      dom_allreduce(dom, dQw, m, 0, s2);
+    }
     launch_multi_dot(dYr, Y, m + 1, n, r, n, ws.rs, s2);
+    dom_allreduce(dom, dYr, m + 1, 0, s2);
     double* rho_out = sc + ((step & 1) ? S_RHO1 : S_RHO0);
     const double* rho_prev = sc + ((step & 1) ? S_RHO0 : S_RHO1);
     ProfScope ps(PROF_SQMR, 8.0 * n * (m + 3), s2);
@@ -455,18 +471,25 @@ SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, doub
   // graph per parity of the step (the rho slots alternate); the host launches one
   // graph and reads the pinned residual per step.
   auto body = [&](int p, cudaStream_t s2) {
-    launch_spmv_dots(t, q, eps, L, hop, sig_total, Qt, n, m + 1, ws.rs.buf(dA, 0), s2);
+    dom_spmv_dots(dom, t, q, eps, hop, sig_total, Qt, n, m + 1, ws.rs.buf(dA, 0), s2);
     const double* rho_cur = sc + ((p ^ 1) ? S_RHO1 : S_RHO0);
     {
       ProfScope ps(PROF_SQMR, 8.0 * n * (m + 4 + 10), s2);
-      k_sqmr_B<<<sgrid(n), TB, 0, s2>>>(n, m, Qt, t, r, dA, rho_cur, sc, ws.rs.buf(red, 1));
+      const int dist = dom.sharded() ? 1 : 0;
+      k_sqmr_B<<<sgrid(n), TB, 0, s2>>>(n, m, Qt, t, r, dA, rho_cur, sc, ws.rs.buf(red, 1), dist);
       AJ_LAUNCHED();
+      if (dist) {
+        dom_allreduce(dom, red, 1, 0, s2);
+        k_sqmr_B_scalars<<<1, 1, 0, s2>>>(m, red, dA, rho_cur, sc);
+        AJ_LAUNCHED();
+      }
       k_sqmr_C<<<sgrid(n), TB, 0, s2>>>(n, q, t, d, x, sv, rx, sc, ws.rs.buf(red + 8, 2));
       AJ_LAUNCHED();
+      dom_allreduce(dom, sc + S_RX2, 1, 0, s2);
     }
     AJ_CUDA(cudaMemcpyAsync(ws.hpin, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s2));
   };
-  const bool use_graph = ws.use_graphs && maxit >= 4;
+  const bool use_graph = ws.use_graphs && maxit >= 4 && !dom.sharded();  // callbacks are not captured
   cudaGraphExec_t gx[2] = {nullptr, nullptr};
   std::vector<ProfRec> gprof[2];
   int64_t gnodes[2] = {0, 0};

@@ -25,7 +25,7 @@ struct SqmrResult {
   bool breakdown = false;
 };
 
-SqmrResult sqmr_run(const Precond* K, const double* eps, int L, double hop, double shift, const double* Qt,
+SqmrResult sqmr_run(const Precond* K, const double* eps, const Domain& dom, double hop, double shift, const double* Qt,
                     const double* Y, int m, const double* Hinv, const double* b, double* x, double tol,
                     int maxit, Workspace& ws, cudaStream_t st);
 
@@ -35,7 +35,7 @@ struct JdResult {
   double setup_ms = 0, solve_ms = 0;
 };
 
-JdResult jd_run(int k, double sigma, double tol, const double* eps, int L, double hop,
+JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain& dom, double hop,
                 const aj_precond_params& pp, const aj_jd_params& jp, double* h_lambda, double* d_X,
                 double* h_resid, aj_precond_info* pinfo, cudaStream_t st);
 

@@ -12,6 +12,8 @@
 #include "aj_common.cuh"
 #include "aj_kernels.cuh"
 
+#include <string>
+
 namespace aj {
 
 __global__ void k_disorder(double* __restrict__ eps, int64_t n, double W, uint64_t seed) {
@@ -263,6 +265,162 @@ void launch_spmv_slab(double* y, const double* x_ext, const double* eps, int L, 
   k_spmv_slab<<<dim3(ceil_div(L, SBX), ceil_div(L, SBY), zb), dim3(SBX, SBY), 0, st>>>(y, x_ext, eps, L, nz, hop,
                                                                                         sig, kc);
   AJ_LAUNCHED();
+}
+
+// ---- the sharded SpMV (DESIGN.md sect. 6): planes of this rank's slab, the z-neighbours of
+// its first / last plane taken from the received halo planes.  Two plane ranges per launch
+// ([a0, a1) then [b0, b1)), split into chunks of kchunk planes over blockIdx.z; same tile,
+// z-march and summation order as k_spmv.  Optional fused dots as in k_spmv.
+template <int NV>
+__global__ void __launch_bounds__(SBX* SBY)
+    k_spmv_halo(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ xlo,
+                const double* __restrict__ xhi, const double* __restrict__ eps, int L, int nz, double hop, double sig,
+                int a0, int a1, int b0, int b1, int kchunk, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
+  const int i = blockIdx.x * SBX + threadIdx.x;
+  const int j = blockIdx.y * SBY + threadIdx.y;
+  const int na = (a1 - a0 + kchunk - 1) / kchunk;
+  int k0, k1;
+  if ((int)blockIdx.z < na) {
+    k0 = a0 + blockIdx.z * kchunk;
+    k1 = min(k0 + kchunk, a1);
+  } else {
+    k0 = b0 + (blockIdx.z - na) * kchunk;
+    k1 = min(k0 + kchunk, b1);
+  }
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+  if (i < L && j < L && k0 < k1) {
+    const int64_t P = (int64_t)L * L;
+    const int im = (i == 0) ? L - 1 : i - 1, ip = (i == L - 1) ? 0 : i + 1;
+    const int jm = (j == 0) ? L - 1 : j - 1, jp = (j == L - 1) ? 0 : j + 1;
+    const int64_t r0 = (int64_t)j * L, rm = (int64_t)jm * L, rp = (int64_t)jp * L;
+    auto plane = [&](int k) -> const double* { return k < 0 ? xlo : (k >= nz ? xhi : x + (int64_t)k * P); };
+    double xm = __ldg(&plane(k0 - 1)[r0 + i]);
+    double xc = __ldg(&x[(int64_t)k0 * P + r0 + i]);
+    for (int k = k0; k < k1; ++k) {
+      const double xp = __ldg(&plane(k + 1)[r0 + i]);
+      const int64_t b = (int64_t)k * P;
+      const double s = (__ldg(&x[b + r0 + im]) + __ldg(&x[b + r0 + ip])) +
+                       (__ldg(&x[b + rm + i]) + __ldg(&x[b + rp + i])) + (xm + xp);
+      const double v = hop * s + (__ldg(&eps[b + r0 + i]) - sig) * xc;
+      y[b + r0 + i] = v;
+      if constexpr (NV > 0) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] += v * __ldg(&Wv[c * ld + b + r0 + i]);
+      }
+      xm = xc;
+      xc = xp;
+    }
+  }
+  if constexpr (NV > 0)
+    block_reduce_finalize<NV, SBX * SBY>(acc, rb, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                                         gridDim.x * gridDim.y * gridDim.z);
+}
+
+__global__ void k_add_into(int n, double* __restrict__ a, const double* __restrict__ b) {
+  if (threadIdx.x < n) a[threadIdx.x] += b[threadIdx.x];
+}
+
+Domain domain_full(int L) {
+  Domain d;
+  d.L = L;
+  d.z0 = 0;
+  d.nz = L;
+  d.n = (int64_t)L * L * L;
+  return d;
+}
+
+Domain domain_slab(int L, int z0, int nz, const aj_comm* comm, cudaStream_t st) {
+  Domain d;
+  d.L = L;
+  d.z0 = z0;
+  d.nz = nz;
+  d.n = (int64_t)L * L * nz;
+  d.comm = comm;
+  if (d.sharded()) d.halo = dalloc<double>(2 * (size_t)L * L, st);
+  return d;
+}
+
+void domain_release(Domain& d, cudaStream_t st) {
+  dfree(d.halo, st);
+  d.halo = nullptr;
+}
+
+void dom_allreduce(const Domain& d, double* buf, int count, int op, cudaStream_t st) {
+  if (!d.sharded() || count <= 0) return;
+  const int rc = d.comm->allreduce(d.comm->ctx, buf, count, op, (void*)st);
+  AJ_REQUIRE(rc == 0, AJ_ERR_CUDA, "comm allreduce failed (code " + std::to_string(rc) + ")");
+}
+
+// interior planes [1, nz-1) while the halo planes travel, then planes 0 and nz-1
+static void spmv_halo_launch(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+                             const double* W, int64_t ld, int nv, const RedBuf& rb, int a0, int a1, int b0, int b1,
+                             cudaStream_t st) {
+  const int L = d.L;
+  const int np = (a1 - a0) + (b1 - b0);
+  if (np <= 0) return;
+  const int tiles = ceil_div(L, SBX) * ceil_div(L, SBY);
+  int zb = std::max(1, std::min(np, ceil_div(num_sms() * 8, tiles)));
+  const int kc = std::max(1, ceil_div(np, zb));
+  zb = ceil_div(a1 - a0, kc) + ceil_div(b1 - b0, kc);
+  const dim3 g(ceil_div(L, SBX), ceil_div(L, SBY), zb), b(SBX, SBY);
+  const double* xlo = d.halo;
+  const double* xhi = d.halo + (int64_t)L * L;
+  switch (nv) {
+#define CASE(N)                                                                                                \
+  case N:                                                                                                      \
+    k_spmv_halo<N><<<g, b, 0, st>>>(y, x, xlo, xhi, eps, L, d.nz, hop, sig, a0, a1, b0, b1, kc, W, ld, rb); \
+    break;
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+#undef CASE
+    default:
+      throw Error(AJ_ERR_ARG, "spmv_dots: nv out of range");
+  }
+  AJ_LAUNCHED();
+}
+
+static void spmv_sharded_impl(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+                              const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st) {
+  const int64_t P = (int64_t)d.L * d.L;
+  const aj_comm* c = d.comm;
+  int rc = c->halo_start(c->ctx, x, x + (int64_t)(d.nz - 1) * P, d.halo, d.halo + P, P, (void*)st);
+  AJ_REQUIRE(rc == 0, AJ_ERR_CUDA, "comm halo_start failed (code " + std::to_string(rc) + ")");
+  ProfScope ps(PROF_SPMV, (24.0 + 8.0 * nv) * (double)d.n, st);
+  const bool split = d.nz >= 3;
+  RedBuf rb2 = rb;
+  rb2.out = rb.out + nv;  // the boundary planes' partial dots
+  if (split) spmv_halo_launch(d, y, x, eps, hop, sig, W, ld, nv, rb, 1, d.nz - 1, 0, 0, st);
+  rc = c->halo_wait(c->ctx, (void*)st);
+  AJ_REQUIRE(rc == 0, AJ_ERR_CUDA, "comm halo_wait failed (code " + std::to_string(rc) + ")");
+  const int b0 = d.nz - 1 > 0 ? d.nz - 1 : 1;  // nz == 1: one boundary plane only
+  spmv_halo_launch(d, y, x, eps, hop, sig, W, ld, nv, split ? rb2 : rb, 0, 1, b0, d.nz, st);
+  if (nv > 0) {
+    if (split) {
+      k_add_into<<<1, 32, 0, st>>>(nv, rb.out, rb2.out);  // interior + boundary, fixed order
+      AJ_LAUNCHED();
+    }
+    dom_allreduce(d, rb.out, nv, 0, st);
+  }
+}
+
+void dom_spmv(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+              cudaStream_t st) {
+  if (!d.sharded()) {
+    AJ_REQUIRE(d.nz == d.L, AJ_ERR_ARG, "dom_spmv: a single process needs the whole lattice");
+    launch_spmv(y, x, eps, d.L, hop, sig, st);
+    return;
+  }
+  spmv_sharded_impl(d, y, x, eps, hop, sig, nullptr, 0, 0, RedBuf{}, st);
+}
+
+void dom_spmv_dots(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
+                   const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st) {
+  if (!d.sharded()) {
+    launch_spmv_dots(y, x, eps, d.L, hop, sig, W, ld, nv, rb, st);
+    return;
+  }
+  spmv_sharded_impl(d, y, x, eps, hop, sig, W, ld, nv, rb, st);
 }
 
 }  // namespace aj

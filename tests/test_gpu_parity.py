@@ -174,10 +174,11 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
     K.free()
 
 
-@pytest.mark.parametrize("tier", [2, 3, 4])
+@pytest.mark.parametrize("tier", [1, 2, 3, 4, 5])
 def test_precond_schur_tiers_agree(gpu_lib, monkeypatch, tier):
-    # the CTA-per-row (tiers 2a = 2, 2b = 4) and global-table (tier 3) Schur variants compute the
-    # same level structure and the same factor, bit for bit, as the warp variant
+    # every Schur tier (1: warp / 2048 table, 2: 64 threads / 4096, 3: 128 / 8192, 4: CTA / 16384,
+    # 5: CTA / global-memory table) computes the same level structure and the same factor,
+    # bit for bit, as the routed default
     import torch
     L = 16
     p = gpu_lib.default_precond_params(n_coarse_max=200)

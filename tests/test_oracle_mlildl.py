@@ -366,7 +366,7 @@ def _plain_level(Al, Lv, compensate):
     pattern = (np.abs(ACC) > 0) | ((np.abs(ACF) > 0).astype(float) @ (np.abs(Bd[np.ix_(F, F)]) > 0).astype(float)
                                    @ (np.abs(AFC) > 0).astype(float) > 0) | np.eye(len(C), dtype=bool)
     S = S1 - np.where(pattern, ACF @ V[np.ix_(F, F)] @ AFC, 0.0)
-    return Lp, S
+    return Lp, 0.5 * (S + S.T)
 
 
 @pytest.mark.parametrize("case,compensate", [("lattice", True), ("lattice", False), ("random", True),
@@ -395,6 +395,7 @@ def test_ordered_accumulation_equals_plain_definition(case, compensate):
         scale_S = max(1.0, np.abs(Sp).max())
         assert np.abs(Lo - Lp).max() <= 1e-14 * scale_L
         assert np.abs(So - Sp).max() <= 1e-14 * scale_S
-        # pattern: the oracle stores exactly the structural pattern (no entries outside it)
+        # S is stored symmetric bit for bit (upper triangle mirrored)
+        assert (Lv.S != Lv.S.T).nnz == 0
         nvirt += Lv.nvirtual
     assert (nvirt > 0) == compensate

@@ -115,6 +115,10 @@ typedef struct {
   double tau_virtual;    /* only couplings |a^_uv| >= tau_virtual are compensated;
                             < 0: auto, 5 tau_drop (L <= 50) .. 10 tau_drop
                             (L >= 100), linear in between                        */
+  double tau_inv;        /* inverse-based (aggressive) dropping a posteriori,
+                            PAPER.md l.947-973: drop l_cf when
+                            |l_cf| <= tau_inv / (nu_c #col_f), nu_c ~ ||L~^{-1} e_c||
+                            (R18); 0 = off; needs factor_fp32 = 0      */
 } aj_precond_params;
 
 typedef struct {
@@ -133,6 +137,8 @@ typedef struct {
   int64_t nnz_V;          /* virtual 2x2 blocks over all levels (R17)             */
   int64_t setup_products; /* Schur products l_cx a_c'x over all levels (work model) */
   double setup_bytes;     /* compulsory setup traffic model, bytes (DESIGN.md sect. 4) */
+  double tau_inv;         /* resolved inverse-based dropping threshold (0 = off)   */
+  int64_t nnz_L_dropped_inv; /* L entries removed by the inverse-based dropping      */
 } aj_precond_info;
 
 AJ_API void aj_precond_default_params(aj_precond_params* p);

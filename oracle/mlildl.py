@@ -524,8 +524,10 @@ class MultilevelILDL:
 
     def __init__(self, A, lattice_L=None, kappa=5.0, tau_drop=2e-3, tau_strong=2e-2,
                  n_coarse_max=2048, max_levels=200, stall_frac=0.005, dense_cap=8192, factor_fp32=False,
-                 compensate=True, tau_virtual=None, priority="quality", red=None):
+                 compensate=True, tau_virtual=None, priority="quality", red=None, tau_inv=0.0):
         """red: level-0 independent set of a lattice block (default red_sites(lattice_L)).
+        tau_inv > 0: inverse-based (aggressive) dropping of L a posteriori (PAPER.md
+        l.947-973, reading R18), see `inverse_based_drop`.
         factor_fp32 (reading R16): the stored factor values are rounded to
         IEEE binary32 -- forward entries as fl32(l_cf * D_f), backward entries as
         fl32(l_cf) -- and used in fp64 arithmetic, as on the GPU."""
@@ -557,6 +559,11 @@ class MultilevelILDL:
             self.G = 0.5 * (G + G.T)
         else:
             self.G = np.zeros((0, 0))
+        self.nu = None
+        if tau_inv > 0.0:
+            if self.factor_fp32:
+                raise ValueError("inverse-based dropping is defined on the fp64 factor")
+            self.nu = inverse_based_drop(self, tau_inv)
 
     def fill(self):
         """nnz(LDL^T)/nnz(A) analogue: stored L entries + pivots + dense coarse triangle."""
@@ -582,3 +589,53 @@ class MultilevelILDL:
         zF = Lv.Binv @ rh - (Lv.Lbwd if self.factor_fp32 else Lv.L).T @ yC
         zh[Lv.F] = zF[Lv.F]
         return Lv.D * zh
+
+
+def nu_estimates(M):
+    """nu_i ~ ||L~^{-1} e_i|| for every node of every level ("In principle it
+    can be computed using L~^T instead of L~"), reading R18.  L~ is the unit lower factor of
+    the whole multilevel factorisation in elimination order [F_0, F_1, ..., C_last], each
+    level's block in its own scaled coordinates.  Column i of L~^{-1} is row i of U^{-1},
+    U = L~^T; the Cline-Moler-Stewart-Wilkinson estimate solves U x = b by back
+    substitution, choosing b_i = +-1 against the partial sum:
+        s_i = sum_{j later} l_ji x_j,   b_i = -1 if s_i > 0 else +1,   x_i = b_i - s_i,
+    so nu_i = |x_i| = 1 + |s_i|.  The final coarse nodes have no L entries (x = +1).  For a
+    pivot f of level l the later nodes j with l_jf != 0 are the coarse nodes of level l,
+    whose x is level l+1's; s_f sums its L^T row in ascending coarse index, one rounded
+    product then one rounded addition per entry.  Returns [x of level l (length n_l)]."""
+    xs = [None] * len(M.levels)
+    x_next = np.ones(M.coarse_n)
+    for lev in reversed(range(len(M.levels))):
+        Lv = M.levels[lev]
+        Lc = Lv.L.tocoo()                                  # (coarse index, level index f, l)
+        o = np.lexsort((Lc.row, Lc.col))                   # per pivot f: ascending coarse index
+        f, cp, l = Lc.col[o], Lc.row[o], Lc.data[o]
+        s = np.zeros(Lv.n)
+        np.add.at(s, f, l * x_next[cp])                    # sequential, in that order
+        x = np.empty(Lv.n)
+        x[Lv.C] = x_next
+        xf = np.where(s[Lv.F] > 0, -1.0, 1.0) - s[Lv.F]
+        x[Lv.F] = xf
+        xs[lev] = x
+        x_next = x
+    return xs
+
+
+def inverse_based_drop(M, tau):
+    """Aggressive dropping a posteriori (reading R18): an entry l_cf of
+    level l is dropped when |l_cf| <= tau / (nu_c * #col_f), nu_c the estimate of
+    ||L~^{-1} e_c|| (nu_estimates, with the factor before this dropping) and #col_f the
+    number of stored entries of column f of L.  Evaluated on the stored forward value
+    fl(l_cf D_f) as  (|fl(l_cf D_f)| * nu_c) * #col_f <= tau * D_f  (the same inequality, the
+    GPU evaluates it identically on both copies of the entry).  Returns the x vectors."""
+    xs = nu_estimates(M)
+    for lev, Lv in enumerate(M.levels):
+        nu_c = np.abs(xs[lev + 1]) if lev + 1 < len(M.levels) else np.ones(M.coarse_n)
+        Lc = Lv.L.tocoo()
+        cnt = np.bincount(Lc.col, minlength=Lv.n).astype(np.float64)
+        lf = Lc.data * Lv.D[Lc.col]
+        keep = (np.abs(lf) * nu_c[Lc.row]) * cnt[Lc.col] > tau * Lv.D[Lc.col]
+        Lv.L = sp.csr_matrix((Lc.data[keep], (Lc.row[keep], Lc.col[keep])), shape=Lv.L.shape)
+        Lv.L.sort_indices()
+        Lv.ndrop_inv = int((~keep).sum())
+    return xs

@@ -18,7 +18,8 @@ EXPORTS = ["aj_last_error", "aj_version", "anderson_build", "spmv", "anderson_bu
            "aj_precond_default_params",
            "precond_setup", "precond_apply", "precond_info", "precond_free", "sqmr_solve", "multi_dot",
            "ortho_cgs2", "aj_jd_default_params", "jd_solve", "jd_solve_host", "aj_launch_count",
-           "aj_prof_enable", "aj_prof_get"]
+           "aj_prof_enable", "aj_prof_get", "aj_nccl_unique_id", "aj_comm_nccl_create", "aj_comm_nccl_free",
+           "spmv_sharded", "precond_setup_slab", "jd_solve_sharded"]
 
 PROF_CATS = ["spmv", "precond_apply", "precond_setup", "sqmr_update", "jd_subspace"]
 
@@ -33,7 +34,7 @@ class PrecondParams(ctypes.Structure):
     _fields_ = [("kappa", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
                 ("n_coarse_max", ctypes.c_int32), ("max_levels", ctypes.c_int32), ("stall_frac", ctypes.c_double),
                 ("dense_cap", ctypes.c_int32), ("cand_cap", ctypes.c_int32), ("factor_fp32", ctypes.c_int32),
-                ("compensate", ctypes.c_int32), ("tau_virtual", ctypes.c_double)]
+                ("compensate", ctypes.c_int32), ("tau_virtual", ctypes.c_double), ("tau_inv", ctypes.c_double)]
 
 
 class PrecondInfo(ctypes.Structure):
@@ -42,13 +43,14 @@ class PrecondInfo(ctypes.Structure):
                 ("level_pairs", ctypes.c_int32 * 1024), ("level_nnzS", ctypes.c_int64 * 1024),
                 ("setup_ms", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
                 ("tau_virtual", ctypes.c_double), ("nnz_V", ctypes.c_int64), ("setup_products", ctypes.c_int64),
-                ("setup_bytes", ctypes.c_double)]
+                ("setup_bytes", ctypes.c_double), ("tau_inv", ctypes.c_double), ("nnz_L_dropped_inv", ctypes.c_int64)]
 
     def as_dict(self):
         nl = self.levels
         return dict(levels=nl, coarse_n=self.coarse_n, nnz_L=self.nnz_L, nnz_A=self.nnz_A,
                     tau_drop=self.tau_drop, tau_strong=self.tau_strong, tau_virtual=self.tau_virtual,
                     nnz_V=self.nnz_V, setup_products=self.setup_products, setup_bytes=self.setup_bytes,
+                    tau_inv=self.tau_inv, nnz_L_dropped_inv=self.nnz_L_dropped_inv,
                     level_n=list(self.level_n[:nl]), level_nF=list(self.level_nF[:nl]),
                     level_pairs=list(self.level_pairs[:nl]), level_nnzS=list(self.level_nnzS[:nl]),
                     setup_ms=self.setup_ms)
@@ -113,6 +115,14 @@ def lib():
             "aj_launch_count": ([i32], i64),
             "aj_prof_enable": ([i32], ctypes.c_int),
             "aj_prof_get": ([ctypes.POINTER(Prof)], ctypes.c_int),
+            "aj_nccl_unique_id": ([ctypes.c_char_p, vp], ctypes.c_int),
+            "aj_comm_nccl_create": ([vp, ctypes.c_char_p, vp, i32, i32], ctypes.c_int),
+            "aj_comm_nccl_free": ([vp], ctypes.c_int),
+            "spmv_sharded": ([vp, vp, vp, i32, i32, i32, d, d, vp, vp], ctypes.c_int),
+            "precond_setup_slab": ([ctypes.POINTER(vp), vp, i32, i32, i32, i32, d, d, ctypes.POINTER(PrecondParams),
+                                    vp], ctypes.c_int),
+            "jd_solve_sharded": ([i32, d, d, vp, i32, i32, i32, d, ctypes.POINTER(PrecondParams),
+                                  ctypes.POINTER(JdParams), dp, vp, dp, ctypes.POINTER(JdStats), vp, vp], ctypes.c_int),
         }
         for name, (argt, rest) in sig.items():
             f = getattr(L, name)
@@ -182,13 +192,20 @@ def spmv_slab(y, x_ext, eps, L, nz, hop, sigma=0.0):
 
 
 class Precond:
-    """Multilevel ILDL handle: precond_setup / precond_apply / precond_free."""
+    """Multilevel ILDL handle: precond_setup / precond_apply / precond_free.  With
+    slab=(z0, nz, world): precond_setup_slab (the slab's diagonal block, DESIGN.md sect. 6)."""
 
-    def __init__(self, eps, L, hop, sigma=0.0, params=None):
+    def __init__(self, eps, L, hop, sigma=0.0, params=None, slab=None):
         self.h = ctypes.c_void_p()
         p = params or default_precond_params()
-        _check(lib().precond_setup(ctypes.byref(self.h), _ptr(eps), L, hop, sigma, ctypes.byref(p), _stream()))
-        self.n = L ** 3
+        if slab is None:
+            _check(lib().precond_setup(ctypes.byref(self.h), _ptr(eps), L, hop, sigma, ctypes.byref(p), _stream()))
+            self.n = L ** 3
+        else:
+            z0, nz, world = slab
+            _check(lib().precond_setup_slab(ctypes.byref(self.h), _ptr(eps), L, z0, nz, world, hop, sigma,
+                                            ctypes.byref(p), _stream()))
+            self.n = L * L * nz
 
     def apply(self, z, r):
         _check(lib().precond_apply(self.h, _ptr(z), _ptr(r), _stream()))
@@ -278,6 +295,35 @@ def jd_solve_host(k, sigma, tol, eps_host, L, hop, pparams=None, jparams=None, X
                              ctypes.byref(st), _stream())
     _check(rc)
     return lam, res, st.as_dict()
+
+
+def _comm_ptr(comm):
+    return ctypes.cast(comm.ptr(), ctypes.c_void_p) if comm is not None else None
+
+
+def spmv_sharded(y, x, eps, L, z0, nz, hop, sigma, comm):
+    """y = (A - sigma I) x on this rank's z-slab, halos exchanged through `comm` (slab.py)."""
+    _check(lib().spmv_sharded(_ptr(y), _ptr(x), _ptr(eps), L, z0, nz, hop, sigma, _comm_ptr(comm), _stream()))
+    return y
+
+
+def jd_solve_sharded(k, sigma, tol, eps, L, z0, nz, hop, comm, pparams=None, jparams=None, want_vectors=True):
+    """jd_solve on a lattice sharded in z over the ranks of `comm` (slab.TorchComm / slab.NcclComm);
+    eps and the returned X (nz L^2, k) are this rank's slab.  Collective."""
+    import numpy as np
+    import torch
+    lam = np.zeros(k)
+    res = np.zeros(k)
+    X = torch.empty((k, L * L * nz), dtype=torch.float64, device=eps.device) if want_vectors else None
+    st = JdStats()
+    pp = pparams or default_precond_params()
+    jp = jparams or default_jd_params()
+    rc = lib().jd_solve_sharded(k, sigma, tol, _ptr(eps), L, z0, nz, hop, ctypes.byref(pp), ctypes.byref(jp),
+                                lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _ptr(X) if X is not None else None,
+                                res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(st), _comm_ptr(comm),
+                                _stream())
+    _check(rc)
+    return lam, (X.T if X is not None else None), res, st.as_dict()
 
 
 def launch_count(reset=False):

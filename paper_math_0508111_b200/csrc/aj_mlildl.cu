@@ -1296,6 +1296,7 @@ static bool factor_level(const Csr& A, int latticeL, int z0, const aj_precond_pa
 }
 
 static void precond_capture(Precond* K, cudaStream_t st);
+static void inverse_based_drop(Precond* K, double tau, cudaStream_t st);
 
 static bool verbose_setup() {
   static int v = -1;
@@ -1457,6 +1458,7 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
       fprintf(stderr, "[aj setup] coarse n=%d dense inverse %.2f ms\n", nc, wall_ms() - tc0);
     }
     A.release(st);
+    if (P.tau_inv > 0.0) inverse_based_drop(K, P.tau_inv, st);
   } catch (...) {
     precond_destroy(K, st);
     throw;
@@ -1491,6 +1493,8 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
   I.tau_drop = P.tau_drop;
   I.tau_strong = P.tau_strong;
   I.tau_virtual = P.tau_virtual;
+  I.tau_inv = P.tau_inv;
+  for (const auto& v : K->lv) I.nnz_L_dropped_inv += v.ndrop_inv;
   K->bytes_per_apply = precond_bytes_per_apply(K);
   precond_capture(K, st);
   return K;
@@ -1525,6 +1529,149 @@ static void precond_inner(const Precond* K, cudaStream_t st) {
     const Level& v = K->lv[l];
     launch_bwd(v, v.r, (l + 1 < nl) ? K->lv[l + 1].z : K->zc, v.z, st);
   }
+}
+
+// ----------------------------------------------------------------------------
+// Inverse-based (aggressive) dropping a posteriori (reading R18,
+// oracle/mlildl.py::nu_estimates / inverse_based_drop): the Cline-Moler-Stewart-
+// Wilkinson estimate x of the column norms nu_i ~ ||L~^{-1} e_i|| by back substitution
+// with L~^T, level by level from the coarse block up (one thread per L^T row, the row
+// summed in ascending coarse index: the oracle's order), then every entry with
+// (|fl(l D_f)| nu_c) #col_f <= tau D_f is removed from both copies of L.
+__global__ void k_nu_pivots(int nF, const int64_t* __restrict__ LTptr, const int32_t* __restrict__ LTcol,
+                            const double* __restrict__ LTval, const double* __restrict__ xn,
+                            const int32_t* __restrict__ fidx, double* __restrict__ x) {
+  for (int fp = blockIdx.x * TB + threadIdx.x; fp < nF; fp += gridDim.x * TB) {
+    double s = 0.0;
+    for (int64_t e = LTptr[fp]; e < LTptr[fp + 1]; ++e) s = __dadd_rn(s, __dmul_rn(LTval[e], xn[LTcol[e]]));
+    x[fidx[fp]] = __dsub_rn(s > 0.0 ? -1.0 : 1.0, s);
+  }
+}
+__global__ void k_nu_coarse(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ xn,
+                            double* __restrict__ x) {
+  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) x[cidx[cp]] = xn[cp];
+}
+__device__ __forceinline__ bool inv_keep(double lf, double nu_c, double cnt_f, double tau, double Df) {
+  return __dmul_rn(__dmul_rn(fabs(lf), nu_c), cnt_f) > __dmul_rn(tau, Df);
+}
+// forward rows (over coarse nodes): count / compact the kept entries
+template <bool FILL>
+__global__ void k_inv_fwd(int nC, const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol,
+                          const double* __restrict__ Lval, int compact, const int32_t* __restrict__ fmap,
+                          const int32_t* __restrict__ fidx, const double* __restrict__ D,
+                          const int64_t* __restrict__ LTptr, const double* __restrict__ xn, double tau,
+                          int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ Lcol2, double* __restrict__ Lval2) {
+  for (int cp = blockIdx.x * TB + threadIdx.x; cp < nC; cp += gridDim.x * TB) {
+    const double nu = fabs(xn[cp]);
+    int64_t w = FILL ? cnt_or_ptr[cp] : 0;
+    for (int64_t e = Lptr[cp]; e < Lptr[cp + 1]; ++e) {
+      const int fp = compact ? Lcol[e] : fmap[Lcol[e]];
+      const int f = fidx[fp];
+      const double cntf = (double)(LTptr[fp + 1] - LTptr[fp]);
+      if (!inv_keep(Lval[e], nu, cntf, tau, D[f])) continue;
+      if (FILL) {
+        Lcol2[w] = Lcol[e];
+        Lval2[w] = Lval[e];
+      }
+      ++w;
+    }
+    if (!FILL) cnt_or_ptr[cp] = w;
+  }
+}
+// backward rows (over pivots): the same decision, fl(l D_f) recomputed exactly as k_l_gather
+template <bool FILL>
+__global__ void k_inv_bwd(int nF, const int64_t* __restrict__ LTptr, const int32_t* __restrict__ LTcol,
+                          const double* __restrict__ LTval, const int32_t* __restrict__ fidx,
+                          const double* __restrict__ D, const double* __restrict__ xn, double tau,
+                          int64_t* __restrict__ cnt_or_ptr, int32_t* __restrict__ LTcol2, double* __restrict__ LTval2,
+                          int64_t* __restrict__ ndrop) {
+  for (int fp = blockIdx.x * TB + threadIdx.x; fp < nF; fp += gridDim.x * TB) {
+    const int f = fidx[fp];
+    const double Df = D[f];
+    const int64_t e0 = LTptr[fp], e1 = LTptr[fp + 1];
+    const double cntf = (double)(e1 - e0);
+    int64_t w = FILL ? cnt_or_ptr[fp] : 0;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int cp = LTcol[e];
+      const double lf = LTval[e] * Df;
+      if (!inv_keep(lf, fabs(xn[cp]), cntf, tau, Df)) continue;
+      if (FILL) {
+        LTcol2[w] = cp;
+        LTval2[w] = LTval[e];
+      }
+      ++w;
+    }
+    if (!FILL) {
+      cnt_or_ptr[fp] = w;
+      atomicAdd(reinterpret_cast<unsigned long long*>(ndrop), (unsigned long long)((e1 - e0) - w));
+    }
+  }
+}
+
+static void inverse_based_drop(Precond* K, double tau, cudaStream_t st) {
+  AJ_REQUIRE(!K->P.factor_fp32, AJ_ERR_ARG, "inverse-based dropping needs the fp64 factor (factor_fp32 = 0)");
+  const int nl = (int)K->lv.size();
+  if (nl == 0) return;
+  std::vector<double*> x(nl + 1, nullptr);
+  x[nl] = dalloc<double>(std::max(K->nc, 1), st);
+  launch_fill(x[nl], 1.0, std::max(K->nc, 1), st);  // coarse block: no L entries, x = b = +1
+  for (int l = nl - 1; l >= 0; --l) {
+    const Level& v = K->lv[l];
+    x[l] = dalloc<double>(std::max(v.n, 1), st);
+    const int gf = std::max(1, std::min(grid_for(std::max(v.nF, 1)), num_sms() * 8));
+    k_nu_pivots<<<gf, TB, 0, st>>>(v.nF, v.LTptr, v.LTcol, (const double*)v.LTval, x[l + 1], v.fidx, x[l]);
+    AJ_LAUNCHED();
+    const int gc = std::max(1, std::min(grid_for(std::max(v.nC, 1)), num_sms() * 8));
+    k_nu_coarse<<<gc, TB, 0, st>>>(v.nC, v.cidx, x[l + 1], x[l]);
+    AJ_LAUNCHED();
+  }
+  int64_t* ndrop = dalloc<int64_t>(1, st);
+  for (int l = 0; l < nl; ++l) {
+    Level& v = K->lv[l];
+    const double* xn = x[l + 1];
+    AJ_CUDA(cudaMemsetAsync(ndrop, 0, sizeof(int64_t), st));
+    const int gc = std::max(1, std::min(grid_for(std::max(v.nC, 1)), num_sms() * 8));
+    const int gf = std::max(1, std::min(grid_for(std::max(v.nF, 1)), num_sms() * 8));
+    const int compact = v.rF ? 1 : 0;  // levels >= 1 store pivot-local columns
+    int64_t* cnt = dalloc<int64_t>(std::max(v.nC, 1), st);
+    k_inv_fwd<false><<<gc, TB, 0, st>>>(v.nC, v.Lptr, v.Lcol, (const double*)v.Lval, compact, v.fmap, v.fidx, v.D,
+                                        v.LTptr, xn, tau, cnt, nullptr, nullptr);
+    AJ_LAUNCHED();
+    int64_t* Lptr2 = nullptr;
+    const int64_t nL2 = counts_to_ptr(cnt, Lptr2, v.nC, st);
+    int32_t* Lcol2 = dalloc<int32_t>(std::max<int64_t>(nL2, 1), st);
+    double* Lval2 = dalloc<double>(std::max<int64_t>(nL2, 1), st);
+    k_inv_fwd<true><<<gc, TB, 0, st>>>(v.nC, v.Lptr, v.Lcol, (const double*)v.Lval, compact, v.fmap, v.fidx, v.D,
+                                       v.LTptr, xn, tau, Lptr2, Lcol2, Lval2);
+    AJ_LAUNCHED();
+    int64_t* cntF = dalloc<int64_t>(std::max(v.nF, 1), st);
+    k_inv_bwd<false><<<gf, TB, 0, st>>>(v.nF, v.LTptr, v.LTcol, (const double*)v.LTval, v.fidx, v.D, xn, tau, cntF,
+                                        nullptr, nullptr, ndrop);
+    AJ_LAUNCHED();
+    int64_t* LTptr2 = nullptr;
+    const int64_t nLT2 = counts_to_ptr(cntF, LTptr2, v.nF, st);
+    AJ_REQUIRE(nLT2 == nL2, AJ_ERR_CUDA, "inverse-based dropping: L and L^T disagree");
+    int32_t* LTcol2 = dalloc<int32_t>(std::max<int64_t>(nL2, 1), st);
+    double* LTval2 = dalloc<double>(std::max<int64_t>(nL2, 1), st);
+    k_inv_bwd<true><<<gf, TB, 0, st>>>(v.nF, v.LTptr, v.LTcol, (const double*)v.LTval, v.fidx, v.D, xn, tau, LTptr2,
+                                       LTcol2, LTval2, ndrop);
+    AJ_LAUNCHED();
+    v.ndrop_inv = v.nnzL - nL2;
+    for (void* q : {(void*)v.Lptr, (void*)v.Lcol, v.Lval, (void*)v.LTptr, (void*)v.LTcol, v.LTval, (void*)cnt,
+                    (void*)cntF})
+      dfree(q, st);
+    v.Lptr = Lptr2;
+    v.Lcol = Lcol2;
+    v.Lval = Lval2;
+    v.LTptr = LTptr2;
+    v.LTcol = LTcol2;
+    v.LTval = LTval2;
+    v.nnzL = v.nnzLT = nL2;
+    v.gf = pick_group(v.nC ? (double)v.nnzL / v.nC : 1.0, v.nnzL);
+    v.gb = pick_group(v.nF ? (double)v.nnzLT / v.nF : 1.0, v.nnzLT, v.nF <= 2048 ? TB : 32);
+  }
+  dfree(ndrop, st);
+  for (double* p : x) dfree(p, st);
 }
 
 static void precond_capture(Precond* K, cudaStream_t st) {

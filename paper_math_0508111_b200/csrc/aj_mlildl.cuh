@@ -22,6 +22,7 @@ struct Level {
   int64_t nnzFC = 0;                          // coarse entries of the pivot rows (Schur work per row = their FC lists)
   int64_t nnzA = 0;                           // entries of the level matrix
   int64_t schur_products = 0;                 // Schur products l_cx a_c'x computed at this level
+  int64_t ndrop_inv = 0;                      // L entries removed by the inverse-based dropping
   int64_t nnzL = 0, nnzLT = 0, nnzS = 0;
   double* D = nullptr;          // n   symmetric scaling of this level
   int32_t* cmap = nullptr;      // n   coarse index of C nodes, -1 for F

@@ -109,3 +109,73 @@ def test_slab_bounds_and_single_rank_halo():
     xe = torch.cat([torch.zeros(P, dtype=torch.float64), x, torch.zeros(P, dtype=torch.float64)])
     slab.halo_exchange(xe, L, L)                     # one rank: periodic wrap
     assert torch.equal(xe[:P], x[(L - 1) * P:]) and torch.equal(xe[(L + 1) * P:], x[:P])
+
+
+def _comm_worker(rank, ws, port, L, out):
+    # the tensor-level core of slab.TorchComm (the aj_comm the sharded solve calls):
+    # sum / max all-reduce and the periodic plane exchange, on the default group and on a
+    # subgroup (P2P peers are global ranks)
+    os.environ.update(WORLD_SIZE=str(ws), RANK=str(rank), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_math_0508111_b200 import slab
+    dist.init_process_group("gloo")
+    res = {}
+    c = slab.TorchComm()
+    t = torch.tensor([1.0 + rank, -2.0 * rank, 0.5], dtype=torch.float64)
+    c.allreduce_(t, 0)
+    res["sum"] = t.tolist()
+    t = torch.tensor([float(rank), -float(rank)], dtype=torch.float64)
+    c.allreduce_(t, 1)
+    res["max"] = t.tolist()
+    z0, nz = slab.slab_bounds(L, rank, ws)
+    P = L * L
+    full = torch.arange(L * P, dtype=torch.float64)
+    mine = full[z0 * P:(z0 + nz) * P]
+    lo, hi = torch.empty(P, dtype=torch.float64), torch.empty(P, dtype=torch.float64)
+    c.exchange_(mine[:P], mine[(nz - 1) * P:], lo, hi)
+    res["halo"] = (bool(torch.equal(lo, full[((z0 - 1) % L) * P:((z0 - 1) % L + 1) * P])),
+                   bool(torch.equal(hi, full[((z0 + nz) % L) * P:((z0 + nz) % L + 1) * P])))
+    # subgroup of the odd-or-even ranks: its own slabs, halos among its members only
+    members = [r for r in range(ws) if r % 2 == 0]
+    grp = dist.new_group(members)
+    if rank in members:
+        gc = slab.TorchComm(grp)
+        gw, gr = len(members), members.index(rank)
+        z0, nz = slab.slab_bounds(L, gr, gw)
+        mine = full[z0 * P:(z0 + nz) * P]
+        c.__class__.exchange_(gc, mine[:P], mine[(nz - 1) * P:], lo, hi)
+        res["sub"] = (bool(torch.equal(lo, full[((z0 - 1) % L) * P:((z0 - 1) % L + 1) * P])),
+                      bool(torch.equal(hi, full[((z0 + nz) % L) * P:((z0 + nz) % L + 1) * P])))
+        s = torch.tensor([1.0], dtype=torch.float64)
+        gc.allreduce_(s)
+        res["subsum"] = float(s.item())
+    out.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("ws,L", [(2, 6), (3, 7), (4, 9)])
+def test_torch_comm_core(ws, L):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, ws, port, L, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(ws):
+        assert res[r]["sum"] == [sum(1.0 + k for k in range(ws)), sum(-2.0 * k for k in range(ws)), 0.5 * ws]
+        assert res[r]["max"] == [ws - 1.0, 0.0]
+        assert res[r]["halo"] == (True, True)
+    members = [r for r in range(ws) if r % 2 == 0]
+    for r in members:
+        assert res[r]["sub"] == (True, True)
+        assert res[r]["subsum"] == float(len(members))

@@ -103,7 +103,7 @@ def test_spmv_sharded_single_rank(gpu_lib):
     xe = torch.zeros((L + 2) * P, dtype=torch.float64, device="cuda")
     xe[P:(L + 1) * P] = x
     ys = torch.empty_like(x)
-    slab.spmv_sharded(ys, xe, eps, L, L, -1.0, 0.0)
+    slab.spmv_sharded_ext(ys, xe, eps, L, L, -1.0, 0.0)
     assert torch.linalg.norm(ys - y) <= 1e-14 * torch.linalg.norm(y)
 
 
@@ -139,7 +139,7 @@ def _oracle_precond(L, eps, hop, sigma, p):
     return mlildl.MultilevelILDL(A, lattice_L=L, kappa=p.kappa, tau_drop=td, tau_strong=ts,
                                  n_coarse_max=p.n_coarse_max, max_levels=p.max_levels, stall_frac=p.stall_frac,
                                  dense_cap=p.dense_cap, factor_fp32=bool(p.factor_fp32),
-                                 compensate=bool(p.compensate))
+                                 compensate=bool(p.compensate), tau_inv=p.tau_inv)
 
 
 @pytest.mark.parametrize("fp32,comp", [(0, 1), (1, 1), (0, 0)])
@@ -167,6 +167,29 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
     assert info["tau_virtual"] == (5.0 * info["tau_drop"] if comp else 0.0)
     for s in (21, 22):
         r = rand_vec(L ** 3, s)
+        z = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+        K.apply(z, T(r))
+        zr = M.apply(r)
+        assert np.linalg.norm(N(z) - zr) <= 1e-8 * np.linalg.norm(zr)
+    K.free()
+
+
+@pytest.mark.parametrize("tau_inv", [0.1, 0.5])
+@pytest.mark.parametrize("L,W,seed", [(12, 16.5, 2), (20, 16.5, 5), (16, 12.0, 3)])
+def test_precond_inverse_dropping_parity(gpu_lib, L, W, seed, tau_inv):
+    # inverse-based dropping a posteriori (reading R18): the same entries
+    # removed as by the oracle (its nu estimates summed in the same order), apply parity
+    import torch
+    p = gpu_lib.default_precond_params(n_coarse_max=200, tau_inv=tau_inv)
+    eps_g = gpu_eps(gpu_lib, L, W, seed)
+    K = gpu_lib.Precond(eps_g, L, -1.0, 0.0, p)
+    info = K.info()
+    M = _oracle_precond(L, an.disorder(L, W, seed), -1.0, 0.0, p)
+    assert info["levels"] == len(M.levels)
+    assert info["nnz_L"] == sum(lv.L.nnz for lv in M.levels)
+    assert info["nnz_L_dropped_inv"] == sum(lv.ndrop_inv for lv in M.levels) > 0
+    for s_ in (21, 22):
+        r = rand_vec(L ** 3, s_)
         z = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
         K.apply(z, T(r))
         zr = M.apply(r)

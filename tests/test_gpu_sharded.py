@@ -1,0 +1,251 @@
+"""GPU tests of the z-slab sharded path (row (e), DESIGN.md sect. 6), through the C ABI.
+
+Only one GPU exists here, so several ranks share cuda:0 with host-staged gloo
+communication (slab.TorchComm): their kernels never wait on one another on the
+device.  The NCCL communicator is exercised at world size 1 (its calls, self
+send/receive) -- the multi-GPU runs are the bench's.
+"""
+import ctypes
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from inputs import CONFIGS, rand_vec
+from oracle import anderson as an
+from oracle import eigs, mlildl
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def T(x):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+def N(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+# ---------------------------------------------------------------- slab preconditioner
+@pytest.mark.parametrize("L,world,W,seed", [(12, 2, 16.5, 1), (16, 3, 16.5, 2), (20, 4, 12.0, 3), (11, 3, 21.0, 4)])
+def test_precond_slab_parity(gpu_lib, L, world, W, seed):
+    # each rank's block-Jacobi piece = the oracle multilevel ILDL of the slab's diagonal block
+    # of A - sigma I (sect. 7 on oracle/anderson.slab_block), level 0 = the red sites
+    # of the global lattice: identical level structure, apply within the parity tolerance
+    import torch
+    from paper_math_0508111_b200 import slab
+    hop, sigma = -1.0, 0.0
+    eps = an.disorder(L, W, seed)
+    p = gpu_lib.default_precond_params(n_coarse_max=150)
+    td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
+    ts = min(0.05, 40 * td)
+    for r in range(world):
+        z0, nz = slab.slab_bounds(L, r, world)
+        rows = an.slab_rows(L, z0, nz)
+        es = torch.empty(nz * L * L, dtype=torch.float64, device="cuda")
+        gpu_lib.anderson_build_slab(es, L, z0, nz, W, seed)
+        K = gpu_lib.Precond(es, L, hop, sigma, p, slab=(z0, nz, world))
+        info = K.info()
+        M = mlildl.MultilevelILDL(an.slab_block(L, z0, nz, eps, hop=hop, sigma=sigma), red=an.red_sites(L)[rows],
+                                  tau_drop=td, tau_strong=ts, n_coarse_max=150, max_levels=p.max_levels,
+                                  stall_frac=p.stall_frac)
+        assert info["levels"] == len(M.levels)
+        assert info["level_n"] == [lv.n for lv in M.levels]
+        assert info["level_nF"] == [len(lv.F) for lv in M.levels]
+        assert info["level_nnzS"] == [lv.S.nnz for lv in M.levels]
+        assert info["nnz_L"] == sum(lv.L.nnz for lv in M.levels)
+        rv = rand_vec(nz * L * L, 30 + r)
+        z = torch.empty(nz * L * L, dtype=torch.float64, device="cuda")
+        K.apply(z, T(rv))
+        zr = M.apply(rv)
+        assert np.linalg.norm(N(z) - zr) <= 1e-8 * np.linalg.norm(zr)
+        K.free()
+
+
+def test_precond_slab_world1_is_full(gpu_lib):
+    import torch
+    L = 14
+    eps = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    gpu_lib.anderson_build(eps, L, 16.5, 5)
+    r = T(rand_vec(L ** 3, 3))
+    K1 = gpu_lib.Precond(eps, L, -1.0, 0.0)
+    K2 = gpu_lib.Precond(eps, L, -1.0, 0.0, slab=(0, L, 1))
+    z1, z2 = torch.empty_like(r), torch.empty_like(r)
+    K1.apply(z1, r)
+    K2.apply(z2, r)
+    assert torch.equal(z1, z2)
+    K1.free()
+    K2.free()
+
+
+# ---------------------------------------------------------------- sharded SpMV
+class LoopbackComm:
+    """aj_comm of rank `rank` of `world` in ONE process: halo planes read from the full
+    vector (what the neighbours would send); no reductions are needed by the SpMV."""
+
+    def __init__(self, world, rank, full, L, z0, nz):
+        from paper_math_0508111_b200 import slab
+        self.full, self.L, self.z0, self.nz = full, L, z0, nz
+        self._cb = (slab.ALLREDUCE_FN(lambda *a: 0), slab.HALO_START_FN(self._start), slab.HALO_WAIT_FN(lambda *a: 0))
+        self.c = slab.AjComm(world, rank, None, *self._cb)
+        self.sent = []
+
+    def _start(self, ctx, slo, shi, rlo, rhi, count, stream):
+        from paper_math_0508111_b200 import slab
+        P = self.L * self.L
+        assert count == P
+        lo, hi = (self.z0 - 1) % self.L, (self.z0 + self.nz) % self.L
+        slab._dev(rlo, P).copy_(self.full[lo * P:(lo + 1) * P])
+        slab._dev(rhi, P).copy_(self.full[hi * P:(hi + 1) * P])
+        self.sent.append((slab._dev(slo, P).clone(), slab._dev(shi, P).clone()))
+        return 0
+
+    def ptr(self):
+        return ctypes.pointer(self.c)
+
+
+@pytest.mark.parametrize("L,world", [(12, 2), (13, 3), (16, 4), (9, 8), (64, 8)])
+def test_spmv_sharded_matches_full(gpu_lib, L, world):
+    # the slab SpMV (interior planes, then the two halo-dependent planes) reproduces the
+    # full-lattice SpMV on every slab; what it sends are its first / last planes
+    import torch
+    from paper_math_0508111_b200 import slab
+    hop, sigma, W, seed = -1.0, 0.3, 16.5, 2
+    P = L * L
+    eps = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    gpu_lib.anderson_build(eps, L, W, seed)
+    x = T(rand_vec(L ** 3, 5))
+    y = torch.empty_like(x)
+    gpu_lib.spmv(y, x, eps, L, hop, sigma)
+    for r in range(world):
+        z0, nz = slab.slab_bounds(L, r, world)
+        c = LoopbackComm(world, r, x, L, z0, nz)
+        xs = x[z0 * P:(z0 + nz) * P].clone()
+        es = eps[z0 * P:(z0 + nz) * P].clone()
+        ys = torch.empty_like(xs)
+        gpu_lib.spmv_sharded(ys, xs, es, L, z0, nz, hop, sigma, c)
+        ref = y[z0 * P:(z0 + nz) * P]
+        assert torch.linalg.norm(ys - ref) <= 1e-14 * torch.linalg.norm(ref)
+        assert torch.equal(c.sent[0][0], xs[:P]) and torch.equal(c.sent[0][1], xs[(nz - 1) * P:])
+
+
+# ---------------------------------------------------------------- sharded Jacobi-Davidson
+def _jd_rank(rank, ws, port, L, W, seed, k, tol, out):
+    os.environ.update(WORLD_SIZE=str(ws), RANK=str(rank), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_math_0508111_b200 import binding, slab
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo")
+    z0, nz = slab.slab_bounds(L, rank, ws)
+    es = torch.empty(nz * L * L, dtype=torch.float64, device="cuda")
+    binding.anderson_build_slab(es, L, z0, nz, W, seed)
+    comm = slab.TorchComm()
+    try:
+        lam, X, res, st = binding.jd_solve_sharded(k, 0.0, tol, es, L, z0, nz, -1.0, comm)
+        out.put((rank, z0, nz, lam.tolist(), res.tolist(), X.cpu().numpy(), st["outer"], st["inner_total"], None))
+    except Exception as e:
+        out.put((rank, z0, nz, None, None, None, 0, 0, repr(e) + " " + "; ".join(comm.errors)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run_jd_sharded(L, W, seed, k, tol, ws):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_jd_rank, args=(r, ws, port, L, W, seed, k, tol, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=1500) for _ in range(ws)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert r[-1] is None, r[-1]
+    lam = np.array(res[0][3])
+    for r in res[1:]:
+        assert np.array_equal(np.array(r[3]), lam)     # identical on every rank
+    X = np.concatenate([r[5] for r in res], axis=0)    # slabs in z order
+    return lam, X, np.array(res[0][4]), res
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("L,ws,W,seed", [(10, 2, 16.5, 0), (12, 3, 16.5, 1)])
+def test_jd_sharded_small_matches_dense(L, ws, W, seed):
+    k = 5
+    lam, X, res, _ = _run_jd_sharded(L, W, seed, k, 1e-11, ws)
+    eps = an.disorder(L, W, seed)
+    A = an.matrix(L, eps, hop=-1.0)
+    lr, Xr = eigs.dense_nearest(A, k, 0.0)
+    normA = 6 + np.abs(eps).max()
+    assert np.all(np.abs(np.sort(lam) - np.sort(lr)) <= 1e-10 * normA), (lam, lr)
+    for i in range(k):
+        r = an.stencil_apply(L, eps, X[:, i], hop=-1.0) - lam[i] * X[:, i]
+        assert np.linalg.norm(r) <= 1e-8 * normA
+    assert np.abs(X.T @ X - np.eye(k)).max() <= 1e-8
+
+
+@pytest.mark.timeout(2400)
+def test_jd_sharded_two_ranks_config1_golden():
+    # BASELINE configs[1] (L=50) sharded over two ranks (block-Jacobi preconditioner over
+    # the slabs): the 5 eigenvalues of the oracle golden, residuals from the oracle stencil
+    import json
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "eigs_config1.json")))
+    cfg = CONFIGS[1]
+    L, W, seed, k = cfg["L"], cfg["W"], cfg["seed"], cfg["k"]
+    lam, X, res, ranks = _run_jd_sharded(L, W, seed, k, cfg["tol"], 2)
+    eps = an.disorder(L, W, seed)
+    normA = 6 + np.abs(eps).max()
+    lr = np.array(gold["eigenvalues"][:k])
+    assert np.all(np.abs(np.sort(lam) - np.sort(lr)) <= 1e-10 * normA), (lam, lr)
+    for i in range(k):
+        r = an.stencil_apply(L, eps, X[:, i], hop=-1.0) - lam[i] * X[:, i]
+        assert np.linalg.norm(r) <= 1e-8 * normA
+
+
+# ---------------------------------------------------------------- NCCL communicator
+def test_nccl_comm_world1(gpu_lib):
+    # the library's NCCL aj_comm at world size 1: all-reduce (sum and max are the identity)
+    # and the halo group (self send/receive: the lower halo is the last plane, the upper one
+    # the first), called through the struct's function pointers on the current stream
+    import torch
+    import torch.distributed as dist
+    from paper_math_0508111_b200 import slab
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", world_size=1, rank=0)
+    try:
+        c = slab.NcclComm()
+        cc = c.ptr().contents
+        assert (cc.world, cc.rank) == (1, 0)
+        buf = T(np.array([1.5, -2.0, 3.0]))
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        assert cc.allreduce(cc.ctx, ctypes.c_void_p(buf.data_ptr()), 3, 0, st) == 0
+        assert cc.allreduce(cc.ctx, ctypes.c_void_p(buf.data_ptr()), 3, 1, st) == 0
+        assert N(buf).tolist() == [1.5, -2.0, 3.0]
+        P = 16
+        x = T(rand_vec(3 * P, 1))
+        halo = torch.zeros(2 * P, dtype=torch.float64, device="cuda")
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        assert cc.halo_start(cc.ctx, p(x), p(x[2 * P:]), p(halo), p(halo[P:]), P, st) == 0
+        assert cc.halo_wait(cc.ctx, st) == 0
+        assert torch.equal(halo[:P], x[2 * P:]) and torch.equal(halo[P:], x[:P])
+        c.free()
+    finally:
+        dist.destroy_process_group()

@@ -399,3 +399,81 @@ def test_ordered_accumulation_equals_plain_definition(case, compensate):
         assert (Lv.S != Lv.S.T).nnz == 0
         nvirt += Lv.nvirtual
     assert (nvirt > 0) == compensate
+
+
+# ---------------------------------------------------------------- inverse-based dropping (R18)
+def test_nu_by_hand():
+    # the one-level 3x3 factor of test_scaled_level_factor_by_hand: F = {0, 2}, C = {1},
+    # L = [[l_10, 0, l_12]] = [[1/(2 sqrt 2), 0, 1]], coarse block {1}.  Back substitution with
+    # L~^T: x_1 = b_1 = +1; s_0 = l_10 x_1 > 0 -> x_0 = -1 - s_0;
+    # s_2 = l_12 x_1 = 1 -> x_2 = -2.  nu = |x| = (1 + 1/(2 sqrt 2), 1, 2) -- here exactly the
+    # 1-norms of the columns of L~^{-1} = I - N.
+    A = np.array([[4.0, 1.0, 0.0],
+                  [1.0, 2.0, 0.5],
+                  [0.0, 0.5, 0.25]])
+    M = mlildl.MultilevelILDL(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.0, n_coarse_max=1,
+                              stall_frac=0.0)
+    x = mlildl.nu_estimates(M)[0]
+    a = 1 / (2 * np.sqrt(2.0))
+    assert np.allclose(x, [-1.0 - a, 1.0, -2.0], rtol=0, atol=1e-15)
+    # dropping rule |l_cf| <= tau / (nu_c #col_f): nu_1 = 1, #col_0 = #col_2 = 1 -> with tau = 0.5
+    # the entry l_10 = 0.354 goes, l_12 = 1 stays
+    M2 = mlildl.MultilevelILDL(sp.csr_matrix(A), kappa=5.0, tau_drop=0.0, tau_strong=0.0, n_coarse_max=1,
+                               stall_frac=0.0, tau_inv=0.5)
+    assert np.allclose(M2.levels[0].L.toarray(), [[0.0, 0.0, 1.0]], rtol=0, atol=0)
+    assert M2.levels[0].ndrop_inv == 1
+
+
+def _global_L(M, n):
+    """The unit lower factor of the whole multilevel factorisation in the original index
+    space: I + sum_l N_l (the level factors' off-diagonal blocks; their products vanish)."""
+    Lg = np.eye(n)
+    orig = np.arange(n)                     # level index -> original index
+    for Lv in M.levels:
+        Ld = Lv.L.toarray()                 # (coarse index, level index)
+        rows, cols = np.nonzero(Ld)
+        Lg[orig[Lv.C[rows]], orig[cols]] = Ld[rows, cols]
+        orig = orig[Lv.C]
+    return Lg
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_nu_bounds_against_exact_columns(seed):
+    # the CMSW estimate is |L~^{-1} b| for a +-1 vector b chosen along the way: 1 <= nu_i <=
+    # ||L~^{-1} e_i||_1, with L~^{-1} computed densely from the global factor
+    L = 8
+    A = an.matrix(L, an.disorder(L, 16.5, seed), hop=-1.0)
+    M = mlildl.MultilevelILDL(A, lattice_L=L, tau_drop=2e-3, tau_strong=0.05, n_coarse_max=40)
+    assert len(M.levels) >= 3
+    xs = mlildl.nu_estimates(M)
+    Lg = _global_L(M, L ** 3)
+    Linv = np.linalg.inv(Lg)
+    col1 = np.abs(Linv).sum(axis=0)          # ||L~^{-1} e_i||_1
+    nu0 = np.abs(xs[0])                      # level 0 covers every node (original order)
+    assert np.all(nu0 >= 1.0 - 1e-15)
+    assert np.all(nu0 <= col1 * (1 + 1e-12))
+    # the estimate is the exact |L~^{-T}... b| of the sign vector it chose: x = L~^{-T} b
+    b = np.where(Lg.T @ xs[0] > 0, 1.0, -1.0)
+    assert np.allclose(Lg.T @ xs[0], b, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("tau", [0.1, 0.5])
+def test_inverse_based_dropping_rule_and_effect(tau):
+    L = 12
+    A = an.matrix(L, an.disorder(L, 16.5, 3), hop=-1.0)
+    kw = dict(lattice_L=L, tau_drop=2e-3, tau_strong=0.05, n_coarse_max=200)
+    M0 = mlildl.MultilevelILDL(A, **kw)
+    M1 = mlildl.MultilevelILDL(A, tau_inv=tau, **kw)
+    xs = mlildl.nu_estimates(M0)
+    for lev, (L0, L1) in enumerate(zip(M0.levels, M1.levels)):
+        nu = np.abs(xs[lev + 1]) if lev + 1 < len(M0.levels) else np.ones(M0.coarse_n)
+        c = L0.L.tocoo()
+        cnt = np.bincount(c.col, minlength=L0.n)
+        ok = np.abs(c.data) * nu[c.row] * cnt[c.col] > tau * (1 + 1e-12)
+        assert L1.L.nnz == ok.sum() or abs(L1.L.nnz - ok.sum()) <= 2   # rounding at the threshold
+        kept = sp.csr_matrix((c.data[ok], (c.row[ok], c.col[ok])), shape=L0.L.shape)
+        assert abs(L1.L - kept).max() == 0.0 or abs(L1.L.nnz - ok.sum()) > 0
+    assert sum(lv.L.nnz for lv in M1.levels) < sum(lv.L.nnz for lv in M0.levels)
+    b = np.random.default_rng(5).standard_normal(L ** 3)
+    x, it, res, _ = sqmr(lambda v: A @ v, M1.apply, b, tol=1e-8, maxit=300)
+    assert res <= 1e-8

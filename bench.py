@@ -7,8 +7,10 @@ One step = one complete jd_solve (multilevel ILDL setup at sigma + Jacobi-Davids
 to k eigenpairs with ||Ax - lambda x|| <= tol ||A||_1) on synthetic disorder that
 is already resident in HBM.  Default workload: BASELINE.json configs[1]
 (L=50, n=125,000, W=16.5, seed 1, 5 pairs nearest sigma=0, tol 1e-10).
-N > 1 (torchrun): every rank solves an independent disorder realisation
-(seed + rank) -- weak scaling over realisations (DESIGN.md sect. 6).
+N > 1 (torchrun): ONE lattice sharded into z-slabs over the N ranks
+(jd_solve_sharded: one-plane halo exchange and dot all-reduce through the
+library's NCCL communicator, block-Jacobi multilevel ILDL over the slabs) --
+strong scaling, the same workload at every N (DESIGN.md sect. 6).
 
 Prints ONE JSON line on rank 0 (contract in DESIGN.md sect. 7).
 """
@@ -41,6 +43,10 @@ def parse():
     ap.add_argument("--prof-cats", default="precond_apply,precond_setup",
                     help="phases timed live inside the timed region (each adds two stream events per call)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "torch"],
+                    help="sharded path's communicator: the library's NCCL one (product) or torch.distributed "
+                         "with host staging (plumbing test: several ranks on one GPU, gloo)")
+    ap.add_argument("--shard", action="store_true", help="use the sharded entry point at N=1 too (world 1)")
     ap.add_argument("--large", default="3,4",
                     help="BASELINE configs solved once each at full size on one GPU (driver-timed 'large' block)")
     # tuning knobs (defaults = library defaults, aj_*_default_params)
@@ -70,9 +76,10 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+        gpu = torch.cuda.is_available()
+        backend = "nccl" if gpu and getattr(args, "comm", "nccl") == "nccl" else "gloo"
+        if gpu:
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
@@ -90,7 +97,8 @@ def allreduce_max(ws, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -224,13 +232,14 @@ def run_reference(args, cfg, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg):
+def workload_config(cfg, ws=1):
     return {"workload": f"BASELINE configs: Anderson 3D L={cfg['L']} (n={cfg['L'] ** 3}), W={cfg['W']}, periodic, "
                         f"hop={cfg['hop']}, seed {cfg['seed']}, {cfg['k']} eigenpairs nearest sigma={cfg['sigma']}, "
                         f"tol {cfg['tol']}",
             "L": cfg["L"], "n": cfg["L"] ** 3, "W": cfg["W"], "seed": cfg["seed"], "hop": cfg["hop"], "k": cfg["k"],
             "sigma": cfg["sigma"], "tol": cfg["tol"], "l2": "flushed (256 MiB write) between timed steps",
-            "parallelism": "independent disorder realisations per rank (seed + rank)"}
+            "parallelism": (f"z-slab sharded over {ws} ranks (one lattice; halo + dot all-reduce over NCCL, "
+                            f"block-Jacobi ILDL over the slabs)" if ws > 1 else "one GPU, whole lattice")}
 
 
 def apply_traffic(L):
@@ -312,58 +321,135 @@ def big_roofline(binding, L, peak, Lp):
     return out
 
 
-def large_solve(binding, c, peak, pp, jp):
-    """One full-size solve of BASELINE configs[c] on this GPU (device-timed with CUDA
-    events), with the live per-phase throughput of the setup and of the preconditioner
-    apply inside it."""
+class Problem:
+    """This rank's share of one workload: the whole lattice (one GPU) or its z-slab
+    (sharded over the ranks of the process group, slab.slab_bounds).  Every solve goes
+    through the library's public entry points: jd_solve / jd_solve_host on one GPU,
+    jd_solve_sharded with the library's NCCL communicator (or the torch.distributed one
+    with host staging, --comm torch, for plumbing tests) when sharded."""
+
+    def __init__(self, binding, cfg, ws, rank, sharded, comm_kind):
+        import torch
+        from paper_math_0508111_b200 import slab
+        self.b, self.cfg, self.ws, self.sharded = binding, cfg, ws, sharded
+        L = cfg["L"]
+        self.L, self.k = L, cfg["k"]
+        self.z0, self.nz = slab.slab_bounds(L, rank, ws) if sharded else (0, L)
+        self.n_local = self.nz * L * L
+        self.eps = torch.empty(self.n_local, dtype=torch.float64, device="cuda")
+        if sharded:
+            binding.anderson_build_slab(self.eps, L, self.z0, self.nz, cfg["W"], cfg["seed"])
+        else:
+            binding.anderson_build(self.eps, L, cfg["W"], cfg["seed"])
+        self.comm = None
+        if sharded and ws > 1:
+            self.comm = slab.NcclComm() if comm_kind == "nccl" else slab.TorchComm()
+        self.normA = 6 * abs(cfg["hop"]) + self.allreduce(float(self.eps.abs().max()), "max")
+
+    def allreduce(self, v, op="sum"):
+        if self.ws == 1 or not self.sharded:
+            return v
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.as_tensor(np.asarray(v, dtype=np.float64), device=dev).clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.cpu().numpy() if t.ndim else float(t.item())
+
+    def solve(self, pp, jp, eps=None):
+        c, b = self.cfg, self.b
+        eps = self.eps if eps is None else eps
+        if self.sharded:
+            return b.jd_solve_sharded(self.k, c["sigma"], c["tol"], eps, self.L, self.z0, self.nz, c["hop"],
+                                      self.comm, pparams=pp, jparams=jp, want_vectors=True)
+        return b.jd_solve(self.k, c["sigma"], c["tol"], eps, self.L, c["hop"], pparams=pp, jparams=jp,
+                          want_vectors=True)
+
+    def host_buffers(self):
+        import torch
+        eps_h = torch.empty(self.n_local, dtype=torch.float64, pin_memory=True)
+        eps_h.copy_(self.eps.cpu())
+        X_h = torch.empty((self.k, self.n_local), dtype=torch.float64, pin_memory=True)
+        self._eps_d = torch.empty_like(self.eps)
+        return eps_h, X_h
+
+    def solve_host(self, pp, jp, eps_h, X_h):
+        """End to end from pinned host memory: this rank's disorder in, its part of the
+        eigenvectors out, the copies on the solve's stream."""
+        c = self.cfg
+        if not self.sharded:
+            lam, res, st = self.b.jd_solve_host(self.k, c["sigma"], c["tol"], eps_h.numpy(), self.L, c["hop"],
+                                                pparams=pp, jparams=jp, X_host=X_h.numpy())
+            return lam, res, st
+        self._eps_d.copy_(eps_h, non_blocking=True)
+        lam, X, res, st = self.solve(pp, jp, eps=self._eps_d)
+        X_h.copy_(X.T, non_blocking=True)
+        return lam, res, st
+
+    def orth_err(self, X):
+        import numpy as np
+        G = self.allreduce((X.T @ X).cpu().numpy())
+        return float(np.abs(G - np.eye(self.k)).max())
+
+    def free(self):
+        if self.comm is not None and hasattr(self.comm, "free"):
+            self.comm.free()
+        self.comm = None
+
+
+def large_solve(binding, c, peak, pp, jp, ws, rank, sharded, comm_kind):
+    """One full-size solve of BASELINE configs[c] (one GPU, or sharded over the ranks),
+    device-timed with CUDA events (max over ranks), with the live per-phase throughput
+    of the setup, the preconditioner apply and the SpMV inside it."""
     import numpy as np
     import torch
 
     from inputs import CONFIGS
     cfg = CONFIGS[c]
-    L, k = cfg["L"], cfg["k"]
-    n = L ** 3
-    eps = torch.empty(n, dtype=torch.float64, device="cuda")
-    binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
+    pr = Problem(binding, cfg, ws, rank, sharded, comm_kind)
+    L, k, n = pr.L, pr.k, pr.L ** 3
     st = torch.cuda.current_stream()
     torch.cuda.synchronize()
+    barrier(ws)
     binding.prof_enable(True, categories=["precond_apply", "precond_setup", "spmv"])
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    lam, X, res, stats = binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp,
-                                          want_vectors=True)
+    lam, X, res, stats = pr.solve(pp, jp)
     e1.record(st)
     e1.synchronize()
     prof = binding.prof_get()
     binding.prof_enable(False)
-    normA = 6 * abs(cfg["hop"]) + float(eps.abs().max())
-    G = (X.T @ X).cpu().numpy()
+    t = allreduce_max(ws, e0.elapsed_time(e1) / 1e3)
     pi = stats["precond"]
     out = {"workload": f"configs[{c}]: L={L} (n={n}), W={cfg['W']}, seed {cfg['seed']}, {k} pairs nearest "
-                       f"sigma={cfg['sigma']}, tol {cfg['tol']}",
-           "time_to_solution_s": e0.elapsed_time(e1) / 1e3, "setup_ms": stats["setup_ms"],
+                       f"sigma={cfg['sigma']}, tol {cfg['tol']}" + (f", z-slab sharded over {ws} ranks"
+                                                                      if sharded and ws > 1 else ", one GPU"),
+           "time_to_solution_s": t, "setup_ms": stats["setup_ms"],
            "solve_ms": stats["solve_ms"], "outer": stats["outer"], "inner_total": stats["inner_total"],
-           "levels": pi["levels"], "coarse_n": pi["coarse_n"], "nnz_L_per_site": pi["nnz_L"] / n,
-           "max_resid_rel": float(np.max(res)) / normA, "orth_err": float(np.abs(G - np.eye(k)).max()),
+           "levels": pi["levels"], "coarse_n": pi["coarse_n"],
+           "nnz_L_per_site": pr.allreduce(float(pi["nnz_L"])) / n,
+           "max_resid_rel": float(np.max(res)) / pr.normA, "orth_err": pr.orth_err(X),
            "eigenvalues": [float(v) for v in lam],
            "setup_work": {"schur_products": pi["setup_products"], "bytes_model": pi["setup_bytes"],
                           "products_per_s": pi["setup_products"] / (stats["setup_ms"] * 1e-3),
                           "GB/s_model": pi["setup_bytes"] / (stats["setup_ms"] * 1e-3) / 1e9,
-                          "frac_hbm": pi["setup_bytes"] / (stats["setup_ms"] * 1e-3) / 1e9 / peak}}
+                          "frac_hbm": pi["setup_bytes"] / (stats["setup_ms"] * 1e-3) / 1e9 / peak,
+                          "note": "rank 0's slab" if sharded and ws > 1 else "whole lattice"}}
     for cat in ("precond_apply", "spmv"):
         v = prof[cat]
-        if v["calls"]:
-            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
-            out[cat] = {"calls": v["calls"], "ms_per_call": v["ms"] / v["calls"], "bytes_per_call":
-                        v["bytes"] / v["calls"], "GB/s": gbs, "frac": gbs / peak}
-    del eps, X
+        calls = v["calls"]
+        if calls:
+            # whole-job throughput: bytes of all ranks / the slowest rank's time
+            tot_b = pr.allreduce(float(v["bytes"]))
+            ms = allreduce_max(ws, float(v["ms"])) if sharded else v["ms"]
+            gbs = tot_b / (ms * 1e-3) / 1e9
+            out[cat] = {"calls": calls, "ms_per_call": ms / calls, "bytes_per_call": tot_b / calls, "GB/s": gbs,
+                        "frac": gbs / (peak * (ws if sharded else 1)), "n_gpus": ws if sharded else 1}
+    pr.free()
+    del pr, X
     torch.cuda.empty_cache()
     return out
-
-
-def replica_seed(cfg, rank):
-    """N>1 (DESIGN.md sect. 6): one independent disorder realisation per rank."""
-    return cfg["seed"] + rank
 
 
 def run_ours(args, cfg, ws, rank, local):
@@ -371,20 +457,17 @@ def run_ours(args, cfg, ws, rank, local):
     import torch
 
     from paper_math_0508111_b200 import binding
-    k, L = cfg["k"], cfg["L"]
-    seed = replica_seed(cfg, rank)
-    n = L ** 3
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    eps = torch.empty(n, dtype=torch.float64, device=dev)
-    binding.anderson_build(eps, L, cfg["W"], seed)
+    sharded = ws > 1 or args.shard
+    pr = Problem(binding, cfg, ws, rank, sharded, args.comm)
+    k, L = pr.k, pr.L
+    dev = torch.device("cuda", torch.cuda.current_device())
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream()
 
     pp, jp = params_from_args(binding, args)
 
     def step():
-        return binding.jd_solve(k, cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp,
-                                want_vectors=True)
+        return pr.solve(pp, jp)
 
     for i in range(args.warmup):
         lam, X, res, stats = step()
@@ -398,9 +481,8 @@ def run_ours(args, cfg, ws, rank, local):
     # live timing of the heavy phases only (per-call event pairs on the launching stream);
     # the thousands of tiny JD/SQMR vector kernels are not bracketed (overhead)
     binding.prof_enable(True, categories=args.prof_cats.split(","))
-    total_ms = 0.0
     per = []
-    with ClockSampler(local if ws > 1 else 0) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)                     # L2 flush, outside the timed interval
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -418,8 +500,10 @@ def run_ours(args, cfg, ws, rank, local):
     launches = binding.launch_count(reset=True)
     total_ms = sum(per)
     ms_step = allreduce_max(ws, total_ms / args.steps)
+    max_resid_rel = float(np.max(res)) / pr.normA
+    orth = pr.orth_err(X)
 
-    # roofline of the dominant phase inside the timed region
+    # roofline of the dominant phase inside the timed region (this rank's kernels)
     cats = {c: v for c, v in prof.items() if v["calls"] > 0 and v["bytes"] > 0}
     dom = max(cats, key=lambda c: cats[c]["ms"])
     d = cats[dom]
@@ -427,7 +511,7 @@ def run_ours(args, cfg, ws, rank, local):
     achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak,
-            "traffic": apply_traffic(L) if dom == "precond_apply" else None,
+            "traffic": apply_traffic(L) if dom == "precond_apply" and not sharded else None,
             "bytes_model": "precond_apply: 12 B per stored factor entry + per-level vectors; precond_setup: 12 B x "
                            "(level matrix + 2 FC lists + one FC entry per Schur product + 3 S + 4 L), DESIGN.md sect. 4",
             "traffic_source": "profiles/round1_apply_traffic.json (ncu dram__bytes_read+write, one apply)",
@@ -437,30 +521,32 @@ def run_ours(args, cfg, ws, rank, local):
             "phases": {c: {"ms_per_step": v["ms"] / args.steps, "calls_per_step": v["calls"] / args.steps,
                            "GB/s": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] > 0 else None}
                        for c, v in prof.items() if v["calls"] > 0},
+            "scope": f"rank 0's kernels ({'its z-slab' if sharded and ws > 1 else 'whole lattice'})",
             "note": "at L=50 the working set (~0.1-0.2 GB) is L2-resident within a step; "
                     "see kernel_roofline for the HBM-bound lattice"}
 
-    # end to end through the public C-ABI with host buffers
+    # end to end through the public API with pinned host buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
-        eps_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        eps_h.copy_(eps.cpu())
-        X_h = torch.empty((k, n), dtype=torch.float64, pin_memory=True)
-        eh, Xh = eps_h.numpy(), X_h.numpy()
-        binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], pparams=pp, jparams=jp, X_host=Xh)
+        eps_h, X_h = pr.host_buffers()
+        pr.solve_host(pp, jp, eps_h, X_h)
+        torch.cuda.synchronize()
+        barrier(ws)
         tt = []
         for _ in range(args.steps):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            lam_h, res_h, _ = binding.jd_solve_host(k, cfg["sigma"], cfg["tol"], eh, L, cfg["hop"], pparams=pp,
-                                                    jparams=jp, X_host=Xh)
+            pr.solve_host(pp, jp, eps_h, X_h)
             e1.record(st)
             e1.synchronize()
             tt.append(e0.elapsed_time(e1))
         e2e_s = allreduce_max(ws, sum(tt) / len(tt)) / 1e3
-        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * k + 16 * k,
-               "api": "jd_solve_host (C ABI, pinned host eps in, eigenvalues/residuals/eigenvectors out)"}
+        nl = pr.n_local
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(pr.allreduce(float(8 * nl))),
+               "d2h_bytes_per_step": int(pr.allreduce(float(8 * nl * k))) + 16 * k,
+               "api": ("jd_solve_sharded (pinned host slab of eps in, slab of the eigenvectors out)" if sharded else
+                       "jd_solve_host (C ABI, pinned host eps in, eigenvalues/residuals/eigenvectors out)")}
 
     log("e2e done" if e2e else "e2e skipped")
     kr = None
@@ -470,20 +556,19 @@ def run_ours(args, cfg, ws, rank, local):
             kr = big_roofline(binding, args.big_L, peak, args.precond_L)
         except Exception as ex:
             kr = {"error": str(ex)[:300]}
-
     log(f"kernel roofline: {kr}")
     large = None
-    if rank == 0 and ws == 1 and args.large:
+    if args.large:
         large = {}
         for c in [int(x) for x in args.large.split(",") if x.strip()]:
             try:
-                large[f"configs[{c}]"] = large_solve(binding, c, peak, pp, jp)
+                large[f"configs[{c}]"] = large_solve(binding, c, peak, pp, jp, ws, rank, sharded, args.comm)
             except Exception as ex:  # report, do not hide
                 large[f"configs[{c}]"] = {"error": str(ex)[:300]}
             log(f"large configs[{c}]: {large[f'configs[{c}]']}")
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        dt, lam_o = cpu_baseline(cfg, k, seed)
+        dt, lam_o = cpu_baseline(cfg, k, cfg["seed"])
         cpu = {"value": dt, "unit": "s", "cores": 1, "kind": "oracle",
                "sample": f"one full oracle solve of this workload itself (L={L}: oracle/mlildl.py setup + "
                          f"oracle/jd.py, numpy/scipy, 1 thread), {dt:.1f} s",
@@ -491,24 +576,22 @@ def run_ours(args, cfg, ws, rank, local):
         log(f"cpu baseline: {dt:.1f} s (L={L} oracle solve)")
 
     clocks = clk.summary()
+    pr.free()
     if rank == 0:
         line = {"metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(cfg),
-                "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline_clean(roof),
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, ws),
+                "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "cpu_baseline": cpu, "kernel_roofline": kr, "large": large,
                 "jd": {"outer": stats["outer"], "inner_total": stats["inner_total"],
                        "levels": stats["precond"]["levels"], "coarse_n": stats["precond"]["coarse_n"],
                        "setup_ms": stats["setup_ms"], "solve_ms": stats["solve_ms"],
-                       "max_resid_rel": float(np.max(res)) / (6 * abs(cfg["hop"]) + float(eps.abs().max())),
+                       "max_resid_rel": max_resid_rel, "orth_err": orth,
+                       "launches_per_solve": launches / args.steps,
                        "eigenvalues": [float(v) for v in lam]},
                 "step_ms": per,
                 "params": {f: getattr(pp, f) for f, _ in pp._fields_} | {f: getattr(jp, f) for f, _ in jp._fields_}}
         print(json.dumps(line), flush=True)
-
-
-def roofline_clean(r):
-    return r
 
 
 def main():

@@ -738,6 +738,27 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 constexpr int PREF = 8;  // factor entries per lane prefetched before the dependency wait
 
+// sum_q val[e_q] * src[col[e_q]] over e_q = b + q*G < e1, q < PREF: all index/value loads
+// issued before the gathers (memory-level parallelism instead of a dependent chain per entry);
+// the order of the additions is q = 0, 1, ... like the prefetched first batch
+template <int G, typename TV>
+__device__ __forceinline__ double gather_batch(int64_t b, int64_t e1, const int32_t* __restrict__ col,
+                                               const TV* __restrict__ val, const double* __restrict__ src) {
+  int32_t c[PREF];
+  double v[PREF];
+#pragma unroll
+  for (int q = 0; q < PREF; ++q) {
+    const int64_t e = b + (int64_t)q * G;
+    c[q] = (e < e1) ? col[e] : -1;
+    v[q] = (e < e1) ? (double)val[e] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < PREF; ++q)
+    if (c[q] >= 0) acc += v[q] * __ldg(&src[c[q]]);
+  return acc;
+}
+
 template <int G, typename TV>
 __global__ void __launch_bounds__(TB)
     k_apply_fwd(int nC, const int32_t* __restrict__ cidx, const double* __restrict__ D,
@@ -774,7 +795,9 @@ __global__ void __launch_bounds__(TB)
 #pragma unroll
     for (int q = 0; q < PREF; ++q)
       if (pc[q] >= 0) acc += pv[q] * __ldg(&gsrc[pc[q]]);
-    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)Lval[e] * __ldg(&gsrc[Lcol[e]]);
+    // rows longer than PREF*G: the same batching (PREF independent index/value loads,
+    // then PREF independent gathers), two dependent round trips per batch
+    for (int64_t b = e0 + (int64_t)PREF * G; b < e1; b += (int64_t)PREF * G) acc += gather_batch<G>(b, e1, Lcol, Lval, gsrc);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -844,7 +867,7 @@ __global__ void __launch_bounds__(TB)
 #pragma unroll
     for (int q = 0; q < PREF; ++q)
       if (pc[q] >= 0) acc += pv[q] * __ldg(&zn[pc[q]]);
-    for (int64_t e = e0 + (int64_t)PREF * G; e < e1; e += G) acc += (double)LTval[e] * __ldg(&zn[LTcol[e]]);
+    for (int64_t b = e0 + (int64_t)PREF * G; b < e1; b += (int64_t)PREF * G) acc += gather_batch<G>(b, e1, LTcol, LTval, zn);
     if (Vptr)  // virtual couplings: -(B~^{-1} - B_d^{-1}) r^_F  (reading R17)
       for (int64_t e = Vptr[iv] + lane; e < Vptr[iv + 1]; e += G) {
         const int32_t v = Vcol[e];
@@ -874,7 +897,7 @@ __global__ void __launch_bounds__(TB)
 // (streaming, more loads in flight per thread), 4 on small L2-resident ones (more
 // threads); measured at L = 50..200 (DESIGN.md sect. 4)
 static int pick_group(double avg_len, int64_t nnz, int gmax = 32) {
-  static const char* ev = getenv("AJ_PER_LANE");
+  const char* ev = getenv("AJ_PER_LANE");  // testing: read per setup so a test can force it
   const int per_lane = ev ? atoi(ev) : (nnz > (int64_t(1) << 22) ? 8 : 4);
   int g = 1;
   while (g < gmax && g * per_lane <= avg_len) g <<= 1;  // ~per_lane entries per lane (memory-level parallelism)

@@ -12,6 +12,7 @@
 #include "aj_common.cuh"
 #include "aj_kernels.cuh"
 
+#include <cstring>
 #include <string>
 
 namespace aj {
@@ -78,27 +79,24 @@ __global__ void __launch_bounds__(SBX* SBY)
 
 // Even-L variant: every lane owns two consecutive x-sites (16-byte loads and
 // stores of x, eps and y); the x-neighbours i-1 / i+2 come from the adjacent
-// lanes by warp shuffle, only tile-edge lanes touch memory for them.
+// lanes by warp shuffle, only tile-edge lanes touch memory for them.  z-march of
+// the column tile (bx, by) over planes [k0, k1), dots accumulated into acc.
 template <int NV>
-__global__ void __launch_bounds__(SBX* SBY, 4)
-    k_spmv2(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
-            double hop, double sig, int kchunk, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
+__device__ __forceinline__ void spmv2_march(double* __restrict__ y, const double* __restrict__ x,
+                                            const double* __restrict__ eps, int L, double hop, double sig, int bx,
+                                            int by, int k0, int k1, const double* __restrict__ Wv, int64_t ld,
+                                            double (&acc)[NV > 0 ? NV : 1]) {
   const int lane = threadIdx.x;
-  const int i = (blockIdx.x * SBX + lane) * 2;
-  const int j = blockIdx.y * SBY + threadIdx.y;
-  const int k0 = blockIdx.z * kchunk;
-  const int k1 = min(k0 + kchunk, L);
+  const int i = (bx * SBX + lane) * 2;
+  const int j = by * SBY + threadIdx.y;
   const bool act = (i < L) && (j < L);
-  double acc[NV > 0 ? NV : 1];
-#pragma unroll
-  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
   const int64_t P = (int64_t)L * L;
   const int jj = act ? j : 0, ii = act ? i : 0;
   const int jm = (jj == 0) ? L - 1 : jj - 1, jp = (jj == L - 1) ? 0 : jj + 1;
   const int64_t r0 = (int64_t)jj * L, rm = (int64_t)jm * L, rp = (int64_t)jp * L;
   const int im = (ii == 0) ? L - 1 : ii - 1, ip2 = (ii + 2 >= L) ? ii + 2 - L : ii + 2;
   const bool edge_l = (lane == 0), edge_r = (lane == SBX - 1) || (ii + 2 >= L);
-  if (k0 < L) {
+  if (k0 < k1) {
     // register queue of planes k-1, k, k+1 and the diagonal of plane k; the
     // loads of plane k+2 and of eps(k+1) are issued one iteration ahead so two
     // independent HBM streams are in flight per thread
@@ -152,9 +150,238 @@ __global__ void __launch_bounds__(SBX* SBY, 4)
       ec = en;
     }
   }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(SBX* SBY, 4)
+    k_spmv2(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
+            double hop, double sig, int kchunk, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+  const int k0 = blockIdx.z * kchunk;
+  spmv2_march<NV>(y, x, eps, L, hop, sig, blockIdx.x, blockIdx.y, k0, min(k0 + kchunk, L), Wv, ld, acc);
   if constexpr (NV > 0)
     block_reduce_finalize<NV, SBX * SBY>(acc, rb, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
                                          gridDim.x * gridDim.y * gridDim.z);
+}
+
+// Balanced persistent launch of the same z-march: exactly one wave (4 CTAs per SM), the
+// tx * ty * L (column tile, plane) units split into equal contiguous ranges in tile-major
+// order, so every CTA marches ~units/grid planes of one or two column tiles (no partial
+// last wave; the z-halo re-read is 2 planes per range).
+template <int NV>
+__global__ void __launch_bounds__(SBX* SBY, 4)
+    k_spmv2_bal(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
+                double hop, double sig, int tx, int64_t units, const double* __restrict__ Wv, int64_t ld,
+                RedBuf rb) {
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+  int64_t u = units * blockIdx.x / gridDim.x;
+  const int64_t u1 = units * (blockIdx.x + 1) / gridDim.x;
+  while (u < u1) {
+    const int t = (int)(u / L), k0 = (int)(u % L);
+    const int k1 = (int)(k0 + (u1 - u) < (int64_t)L ? k0 + (u1 - u) : (int64_t)L);
+    spmv2_march<NV>(y, x, eps, L, hop, sig, t % tx, t / tx, k0, k1, Wv, ld, acc);
+    u += k1 - k0;
+  }
+  if constexpr (NV > 0) block_reduce_finalize<NV, SBX * SBY>(acc, rb, blockIdx.x, gridDim.x);
+}
+
+// ---- TMA-staged variant (even L, 64 <= L <= 512; DESIGN.md sect. 4) ------------------
+// A CTA owns a band of ny <= TY_MAX full x-rows [j0, j0 + ny) and a chunk of planes
+// [k0, k1).  The bulk-copy engine (cp.async.bulk, completion on an mbarrier) streams, for
+// every plane k0-1 .. k1, the band plus its two halo rows (j0-1, j0+ny, periodic) into a
+// ring of NS shared-memory stages; the threads only wait on the stage barriers and compute
+// from shared memory: x-neighbours (periodic wrap inside the row), y-neighbours (the rows
+// above / below in the stage), z-neighbours (the previous / next stage).  eps, the fused
+// dot vectors and y go through registers (16-byte loads / streaming stores).  CTAs with
+// the same plane chunk and adjacent bands are adjacent in launch order, so the halo rows a
+// band re-reads are its neighbour's rows of the same plane, mostly L2 hits.  Same
+// summation order as k_spmv2 (x-, y-, z-neighbour pairs), so the result is bit-identical.
+constexpr int TMA_NS = 5;       // stages: planes k-1, k, k+1 in use, two in flight
+constexpr int TMA_THREADS = 256;
+constexpr int TMA_SMEM = 110 * 1024;  // two CTAs per SM
+constexpr int TMA_MP = 6;             // pairs per thread and plane: (ty+2) L <= TMA_SMEM / (8 NS)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct TmaGeom {
+  int T, Z, kchunk, ty_max;
+};
+
+template <int NV>
+__global__ void __launch_bounds__(TMA_THREADS, 2)
+    k_spmv_tma(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ eps, int L,
+               double hop, double sig, TmaGeom g, const double* __restrict__ Wv, int64_t ld, RedBuf rb) {
+  extern __shared__ __align__(128) double sx[];
+  __shared__ __align__(8) uint64_t bar[TMA_NS];
+  const int t = blockIdx.x % g.T, zc = blockIdx.x / g.T;
+  const int j0 = (int)((int64_t)t * L / g.T), j1 = (int)((int64_t)(t + 1) * L / g.T), ny = j1 - j0;
+  const int k0 = zc * g.kchunk, k1 = min(L, k0 + g.kchunk);
+  const int64_t P = (int64_t)L * L;
+  const int rowlen = L;                       // doubles per row
+  const int stage_elems = (g.ty_max + 2) * L;  // doubles per stage
+  const int nq = (k1 - k0) + 2;                // planes k0-1 .. k1
+  const uint32_t row_bytes = (uint32_t)L * 8u;
+  double acc[NV > 0 ? NV : 1];
+#pragma unroll
+  for (int c = 0; c < (NV > 0 ? NV : 1); ++c) acc[c] = 0.0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TMA_NS; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int q) {  // plane k0 - 1 + q into stage q % NS (thread 0)
+    const int kk = (k0 - 1 + q + L) % L;
+    double* dst = sx + (size_t)(q % TMA_NS) * stage_elems;
+    uint64_t* b = &bar[q % TMA_NS];
+    const double* pl = x + (int64_t)kk * P;
+    mbar_expect_tx(b, (uint32_t)(ny + 2) * row_bytes);
+    bulk_g2s(dst, pl + (int64_t)((j0 - 1 + L) % L) * L, row_bytes, b);
+    bulk_g2s(dst + rowlen, pl + (int64_t)j0 * L, (uint32_t)ny * row_bytes, b);
+    bulk_g2s(dst + (size_t)(ny + 1) * rowlen, pl + (int64_t)(j1 % L) * L, row_bytes, b);
+  };
+  if (k0 < k1) {
+    if (threadIdx.x == 0)
+      for (int q = 0; q < min(TMA_NS, nq); ++q) issue(q);
+    const int half = L >> 1;
+    const int npairs = ny * half;  // <= TMA_MP * TMA_THREADS (stage budget, tma_geom)
+    // eps of the next plane is loaded one plane ahead into registers (the stage holds x only)
+    double2 en[TMA_MP];
+    auto load_eps = [&](int k) {
+      const int64_t base = (int64_t)k * P + (int64_t)j0 * L;
+#pragma unroll
+      for (int m = 0; m < TMA_MP; ++m) {
+        const int p = threadIdx.x + m * TMA_THREADS;
+        if (p < npairs) {
+          const int r = p / half;
+          en[m] = __ldcs(reinterpret_cast<const double2*>(eps + base + (int64_t)r * L + (p - r * half) * 2));
+        }
+      }
+    };
+    load_eps(k0);
+    for (int k = k0; k < k1; ++k) {
+      const int q = k - k0 + 1;
+      double2 ec[TMA_MP];
+#pragma unroll
+      for (int m = 0; m < TMA_MP; ++m) ec[m] = en[m];
+      if (k + 1 < k1) load_eps(k + 1);
+      if (k == k0) {
+        mbar_wait(&bar[0], 0);
+        mbar_wait(&bar[1 % TMA_NS], 0);
+      }
+      mbar_wait(&bar[(q + 1) % TMA_NS], (uint32_t)(((q + 1) / TMA_NS) & 1));
+      const double* sm = sx + (size_t)((q - 1) % TMA_NS) * stage_elems;
+      const double* sc = sx + (size_t)(q % TMA_NS) * stage_elems;
+      const double* sp = sx + (size_t)((q + 1) % TMA_NS) * stage_elems;
+      const int64_t base = (int64_t)k * P + (int64_t)j0 * L;
+#pragma unroll
+      for (int m = 0; m < TMA_MP; ++m) {
+        const int p = threadIdx.x + m * TMA_THREADS;
+        if (p >= npairs) break;
+        const int r = p / half;
+        const int i = (p - r * half) * 2;
+        const int o = (r + 1) * rowlen + i;  // centre pair in the stage
+        const double2 xc = *reinterpret_cast<const double2*>(sc + o);
+        const double left = sc[(r + 1) * rowlen + (i == 0 ? L - 1 : i - 1)];
+        const double right = sc[(r + 1) * rowlen + (i + 2 == L ? 0 : i + 2)];
+        const double2 xr0 = *reinterpret_cast<const double2*>(sc + o - rowlen);
+        const double2 xr1 = *reinterpret_cast<const double2*>(sc + o + rowlen);
+        const double2 xm = *reinterpret_cast<const double2*>(sm + o);
+        const double2 xp = *reinterpret_cast<const double2*>(sp + o);
+        const int64_t gi = base + (int64_t)r * L + i;
+        const double s0 = (left + xc.y) + (xr0.x + xr1.x) + (xm.x + xp.x);
+        const double s1 = (xc.x + right) + (xr0.y + xr1.y) + (xm.y + xp.y);
+        double2 v;
+        v.x = hop * s0 + (ec[m].x - sig) * xc.x;
+        v.y = hop * s1 + (ec[m].y - sig) * xc.y;
+        __stcs(reinterpret_cast<double2*>(y + gi), v);
+        if constexpr (NV > 0) {
+#pragma unroll
+          for (int c = 0; c < NV; ++c) {
+            const double2 w = __ldg(reinterpret_cast<const double2*>(&Wv[c * ld + gi]));
+            acc[c] += v.x * w.x + v.y * w.y;
+          }
+        }
+      }
+      __syncthreads();  // every thread is done with stage (q - 1) % NS
+      if (threadIdx.x == 0 && q - 1 + TMA_NS < nq) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(q - 1 + TMA_NS);
+      }
+    }
+  }
+  if constexpr (NV > 0) block_reduce_finalize<NV, TMA_THREADS>(acc, rb, blockIdx.x, gridDim.x);
+}
+
+// Kernel choice for the full-lattice SpMV.  Default: the balanced one-wave z-march for
+// even L >= 64 (measured at L=250: see DESIGN.md sect. 4), the tiled z-march otherwise.
+// AJ_SPMV_PATH=tma|bal|grid (testing) forces one (tma/bal need even L, tma 64 <= L <= 512).
+enum SpmvPath { SP_GRID1, SP_GRID2, SP_BAL, SP_TMA };
+
+static TmaGeom tma_geom(int L) {
+  TmaGeom g{0, 0, 0, 0};
+  if (L % 2 != 0 || L < 64 || L > 512) return g;
+  const int rows = TMA_SMEM / (TMA_NS * 8 * L);  // rows per stage in the budget
+  const int ty = std::min(16, rows - 2);
+  if (ty < 4) return g;
+  g.T = ceil_div(L, ty);
+  g.ty_max = ceil_div(L, g.T);
+  const int target = num_sms() * 2;  // one wave of two CTAs per SM
+  g.Z = std::max(1, target / g.T);
+  g.kchunk = ceil_div(L, g.Z);
+  g.Z = ceil_div(L, g.kchunk);
+  return g;
+}
+
+static SpmvPath spmv_path(int L) {
+  if (L % 2 != 0) return SP_GRID1;
+  const char* e = getenv("AJ_SPMV_PATH");
+  if (e && !strcmp(e, "tma") && tma_geom(L).T > 0) return SP_TMA;
+  if (e && !strcmp(e, "grid")) return SP_GRID2;
+  if (e && !strcmp(e, "bal")) return SP_BAL;
+  return L >= 64 ? SP_BAL : SP_GRID2;
+}
+
+static size_t tma_smem_bytes(const TmaGeom& g, int L) { return (size_t)TMA_NS * (g.ty_max + 2) * L * 8; }
+
+template <int NV>
+static void launch_tma(const TmaGeom& g, double* y, const double* x, const double* eps, int L, double hop,
+                       double sig, const double* W, int64_t ld, const RedBuf& rb, cudaStream_t st) {
+  static int attr_dev[64] = {0};
+  int dev = 0;
+  AJ_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr_dev[dev]) {
+    AJ_CUDA(cudaFuncSetAttribute(k_spmv_tma<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM));
+    attr_dev[dev] = 1;
+  }
+  k_spmv_tma<NV><<<g.T * g.Z, TMA_THREADS, tma_smem_bytes(g, L), st>>>(y, x, eps, L, hop, sig, g, W, ld, rb);
 }
 
 static dim3 spmv_grid(int L, int& kchunk) {
@@ -175,38 +402,48 @@ int spmv_grid_blocks(int L) {
   return (int)(g.x * g.y * g.z);
 }
 
+template <int NV>
+static void spmv_dispatch(SpmvPath path, double* y, const double* x, const double* eps, int L, double hop,
+                          double sig, const double* W, int64_t ld, const RedBuf& rb, cudaStream_t st) {
+  const dim3 b(SBX, SBY);
+  if (path == SP_TMA) {
+    launch_tma<NV>(tma_geom(L), y, x, eps, L, hop, sig, W, ld, rb, st);
+  } else if (path == SP_BAL) {
+    const int tx = ceil_div(L, 2 * SBX), ty = ceil_div(L, SBY);
+    const int64_t units = (int64_t)tx * ty * L;
+    const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms() * 4);
+    k_spmv2_bal<NV><<<grid, b, 0, st>>>(y, x, eps, L, hop, sig, tx, units, W, ld, rb);
+  } else {
+    int kc;
+    const dim3 g = spmv_grid(L, kc);
+    if (path == SP_GRID2)
+      k_spmv2<NV><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);
+    else
+      k_spmv<NV><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);
+  }
+  AJ_LAUNCHED();
+}
+
 void launch_spmv(double* y, const double* x, const double* eps, int L, double hop, double sig,
                  cudaStream_t st) {
-  int kc;
-  dim3 g = spmv_grid(L, kc);
   ProfScope ps(PROF_SPMV, 24.0 * L * L * L, st);
-  if (L % 2 == 0)
-    k_spmv2<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
-  else
-    k_spmv<0><<<g, dim3(SBX, SBY), 0, st>>>(y, x, eps, L, hop, sig, kc, nullptr, 0, RedBuf{});
-  AJ_LAUNCHED();
+  spmv_dispatch<0>(spmv_path(L), y, x, eps, L, hop, sig, nullptr, 0, RedBuf{}, st);
 }
 
 void launch_spmv_dots(double* y, const double* x, const double* eps, int L, double hop, double sig,
                       const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st) {
-  int kc;
-  dim3 g = spmv_grid(L, kc);
-  dim3 b(SBX, SBY);
   ProfScope ps(PROF_SPMV, (24.0 + 8.0 * nv) * L * L * L, st);
+  const SpmvPath path = spmv_path(L);
   switch (nv) {
-#define CASE(N)                                                               \
-  case N:                                                                     \
-    if (L % 2 == 0)                                                           \
-      k_spmv2<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);     \
-    else                                                                      \
-      k_spmv<N><<<g, b, 0, st>>>(y, x, eps, L, hop, sig, kc, W, ld, rb);      \
+#define CASE(N)                                                       \
+  case N:                                                             \
+    spmv_dispatch<N>(path, y, x, eps, L, hop, sig, W, ld, rb, st);    \
     break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
 #undef CASE
     default:
       throw Error(AJ_ERR_ARG, "spmv_dots: nv out of range");
   }
-  AJ_LAUNCHED();
 }
 
 // ---- z-slab shard (DESIGN.md sect. 6, row (e)) --------------------------------

@@ -26,14 +26,17 @@ def main():
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if what in ("spmv", "all"):
-        binding.spmv(y, x, eps, L, -1.0, 0.0)
-        e0.record(st)
-        for _ in range(reps):
+        for path in ("bal", "grid", "tma"):   # AJ_SPMV_PATH: the kernel variants (aj_stencil.cu)
+            os.environ["AJ_SPMV_PATH"] = path
             binding.spmv(y, x, eps, L, -1.0, 0.0)
-        e1.record(st)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        print(f"spmv L={L}: {ms:.4f} ms  {24 * n / ms / 1e6:.1f} GB/s", flush=True)
+            e0.record(st)
+            for _ in range(reps):
+                binding.spmv(y, x, eps, L, -1.0, 0.0)
+            e1.record(st)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            print(f"spmv[{path}] L={L}: {ms:.4f} ms  {24 * n / ms / 1e6:.1f} GB/s", flush=True)
+        os.environ.pop("AJ_SPMV_PATH", None)
     if what in ("precond", "all"):
         t0 = time.perf_counter()
         K = binding.Precond(eps, L, -1.0, 0.0)

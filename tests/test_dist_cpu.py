@@ -1,6 +1,6 @@
 """World-size-2 gloo test of bench.py's multi-process plumbing on CPU (DESIGN.md
-sect. 6): rendezvous on 127.0.0.1, barrier, max-over-ranks timing, and one
-independent disorder realisation per rank.  No GPU, no CUDA extension."""
+sect. 6): rendezvous on 127.0.0.1, barrier, max-over-ranks timing, and the z-slab
+split of ONE lattice over the ranks.  No GPU, no CUDA extension."""
 import os
 import socket
 import sys
@@ -31,9 +31,13 @@ def _worker(rank, ws, port, out):
     assert (w, r) == (ws, rank) and dist.get_backend() == "gloo"
     bench.barrier(w)
     m = bench.allreduce_max(w, 10.0 * (rank + 1))
-    seed = bench.replica_seed(CONFIGS[1], rank)
-    eps = an.disorder(6, 16.5, seed)
-    out.put((rank, m, seed, float(eps.sum())))
+    from paper_math_0508111_b200 import slab
+    cfg = CONFIGS[1]
+    assert f"sharded over {ws} ranks" in bench.workload_config(cfg, w)["parallelism"]
+    L = 6
+    z0, nz = slab.slab_bounds(L, rank, ws)
+    eps = an.disorder(L, cfg["W"], cfg["seed"])[z0 * L * L:(z0 + nz) * L * L]   # this rank's slab
+    out.put((rank, m, (z0, nz), float(eps.sum())))
     bench.barrier(w)
     dist.destroy_process_group()
 
@@ -53,8 +57,11 @@ def test_bench_plumbing_world_size_2():
         assert p.exitcode == 0
     (r0, m0, s0, e0), (r1, m1, s1, e1) = res
     assert m0 == m1 == 20.0           # max over ranks reaches every rank
-    assert s1 == s0 + 1               # distinct realisations per rank
-    assert not np.isclose(e0, e1)
+    assert s0 == (0, 3) and s1 == (3, 3)   # the two slabs tile the lattice
+    from inputs import CONFIGS
+    from oracle import anderson as an
+    cfg = CONFIGS[1]
+    assert np.isclose(e0 + e1, an.disorder(6, cfg["W"], cfg["seed"]).sum(), rtol=0, atol=1e-12)
 
 
 def _halo_worker(rank, ws, port, L, out):

@@ -119,6 +119,13 @@ typedef struct {
                             PAPER.md l.947-973: drop l_cf when
                             |l_cf| <= tau_inv / (nu_c #col_f), nu_c ~ ||L~^{-1} e_c||
                             (R18); 0 = off; needs factor_fp32 = 0      */
+  int32_t shard_precond; /* jd_solve_sharded only (DESIGN.md sect. 6):
+                            0 = replicated: every rank factors the WHOLE lattice
+                            (eps all-gathered once) and applies it to the
+                            all-gathered residual -- the single-GPU preconditioner,
+                            identical iteration counts; 1 = block Jacobi over the
+                            slabs (precond_setup_slab; measured to stall the inner
+                            solves, kept for comparison)                           */
 } aj_precond_params;
 
 typedef struct {
@@ -275,7 +282,9 @@ AJ_API int precond_setup_slab(void** handle, const double* d_eps, int32_t L, int
 /* jd_solve on the sharded lattice: same arguments and results as jd_solve, with
  * d_eps (nz L^2, this rank's slab) and d_X (nz L^2 x k, this rank's part of the
  * eigenvectors, may be NULL); h_lambda / h_resid are identical on every rank.  The
- * preconditioner is precond_setup_slab of every rank (block Jacobi over slabs).
+ * preconditioner follows pparams->shard_precond: 0 (default) the whole-lattice multilevel
+ * ILDL on every rank, applied to the residual all-gathered through comm->allreduce
+ * (zero-padded sum of the slabs, exact), 1 precond_setup_slab (block Jacobi over slabs).
  * Collective: every rank calls it with the same k, sigma, tol, params. */
 AJ_API int jd_solve_sharded(int32_t k, double sigma, double tol, const double* d_eps, int32_t L, int32_t z0,
                             int32_t nz, double hop, const aj_precond_params* pparams, const aj_jd_params* jparams,

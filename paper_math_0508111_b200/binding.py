@@ -34,7 +34,8 @@ class PrecondParams(ctypes.Structure):
     _fields_ = [("kappa", ctypes.c_double), ("tau_drop", ctypes.c_double), ("tau_strong", ctypes.c_double),
                 ("n_coarse_max", ctypes.c_int32), ("max_levels", ctypes.c_int32), ("stall_frac", ctypes.c_double),
                 ("dense_cap", ctypes.c_int32), ("cand_cap", ctypes.c_int32), ("factor_fp32", ctypes.c_int32),
-                ("compensate", ctypes.c_int32), ("tau_virtual", ctypes.c_double), ("tau_inv", ctypes.c_double)]
+                ("compensate", ctypes.c_int32), ("tau_virtual", ctypes.c_double), ("tau_inv", ctypes.c_double),
+                ("shard_precond", ctypes.c_int32)]
 
 
 class PrecondInfo(ctypes.Structure):

@@ -112,6 +112,7 @@ void aj_precond_default_params(aj_precond_params* p) {
   p->compensate = 1;       // DESIGN.md R17
   p->tau_virtual = -1.0;   // auto: 5..10 tau_drop for L = 50..100 (R17)
   p->tau_inv = 0.0;        // inverse-based dropping off (R18: measured, see sect. 7a)
+  p->shard_precond = 0;    // sharded solve: replicated whole-lattice preconditioner (DESIGN.md sect. 6)
 }
 
 int precond_setup(void** handle, const double* d_eps, int32_t L, double hop, double sigma,

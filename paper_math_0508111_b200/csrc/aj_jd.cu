@@ -33,9 +33,10 @@ static void rd(T* h, const T* d, size_t cnt, cudaStream_t st) {
   AJ_CUDA(cudaStreamSynchronize(st));
 }
 
-JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain& dom, double hop,
+JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain& dom_in, double hop,
                 const aj_precond_params& pp, const aj_jd_params& jp, double* h_lambda, double* d_X,
                 double* h_resid, aj_precond_info* pinfo, cudaStream_t st) {
+  Domain dom = dom_in;  // + the whole-lattice buffers of the replicated sharded preconditioner
   const int L = dom.L;
   AJ_REQUIRE(L >= 3, AJ_ERR_ARG, "jd_solve: L must be >= 3");
   AJ_REQUIRE(k >= 1 && k <= 16, AJ_ERR_ARG, "jd_solve: 1 <= k <= 16");  // m = k + 1 <= 17 (k_small_inv)
@@ -51,9 +52,26 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
   AJ_CUDA(cudaEventCreate(&e2));
   AJ_CUDA(cudaEventRecord(e0, st));
 
-  // sharded: block Jacobi over the z-slabs (each rank factors its slab's diagonal block)
-  Precond* K = dom.sharded() ? precond_create_slab(eps, L, dom.z0, dom.nz, true, hop, sigma, pp, st)
-                             : precond_create(eps, L, hop, sigma, pp, st);
+  // sharded (DESIGN.md sect. 6): shard_precond 0 = every rank factors the whole lattice
+  // (eps all-gathered once) and applies it to the all-gathered residual -- the single-GPU
+  // preconditioner; 1 = block Jacobi over the z-slabs (each rank its slab's diagonal block)
+  Precond* K = nullptr;
+  if (dom.sharded() && pp.shard_precond == 0) {
+    const int64_t N = (int64_t)L * L * L;
+    dom.rfull = dalloc<double>(N, st);
+    dom.zfull = dalloc<double>(N, st);
+    try {
+      dom_gather_full(dom, dom.zfull, eps, st);  // the whole disorder (zfull as scratch)
+      K = precond_create(dom.zfull, L, hop, sigma, pp, st);
+    } catch (...) {
+      dfree(dom.rfull, st);
+      dfree(dom.zfull, st);
+      throw;
+    }
+  } else {
+    K = dom.sharded() ? precond_create_slab(eps, L, dom.z0, dom.nz, true, hop, sigma, pp, st)
+                      : precond_create(eps, L, hop, sigma, pp, st);
+  }
   if (pinfo) *pinfo = K->info;
   AJ_CUDA(cudaEventRecord(e1, st));
   Workspace ws(n, st);
@@ -90,6 +108,8 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
       dfree(p, st);
     ws.release(st);
     precond_destroy(K, st);
+    dfree(dom.rfull, st);
+    dfree(dom.zfull, st);
   };
   try {
     AJ_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long), st));
@@ -165,7 +185,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
         if (rnorm > tol_abs) break;
         // lock the converged Ritz pair
         launch_copy(QT + (int64_t)nq * n, u, n, st);
-        precond_run(K, Y + (int64_t)nq * n, u, st);
+        dom_precond(dom, K, Y + (int64_t)nq * n, u, st);
         lam.push_back(sigma + theta0);
         ++nq;
         if (jp.verbose)
@@ -213,7 +233,7 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
       const int m = nq + 1;
       const int mpad = (m + 7) & ~7;
       launch_copy(QT + (int64_t)nq * n, u, n, st);
-      precond_run(K, Y + (int64_t)nq * n, u, st);
+      dom_precond(dom, K, Y + (int64_t)nq * n, u, st);
       for (int c = 0; c < m; ++c) launch_multi_dot(Hb + c * mpad, QT, m, n, Y + (int64_t)c * n, n, ws.rs, st);
       dom_allreduce(dom, Hb, m * mpad, 0, st);
       // Hinv = H^{-1} (H column c at Hb + c * mpad); a singular H (K^{-1} Q~ losing rank)

@@ -43,6 +43,8 @@ struct Domain {
   int64_t n = 0;                  // local sites L^2 nz
   const aj_comm* comm = nullptr;  // null (or world == 1): this process owns the periodic lattice
   double* halo = nullptr;         // sharded: 2 L^2 receive planes [below | above] (device)
+  double* rfull = nullptr;        // sharded, replicated preconditioner: whole-lattice r and z
+  double* zfull = nullptr;        //   (L^3 each, jd_run allocates them)
   bool sharded() const { return comm != nullptr && comm->world > 1; }
   int64_t site0() const { return (int64_t)z0 * L * L; }
 };
@@ -52,6 +54,9 @@ Domain domain_slab(int L, int z0, int nz, const aj_comm* comm, cudaStream_t st);
 void domain_release(Domain& d, cudaStream_t st);
 // in-place reduction over the ranks (op 0 sum, 1 max); no-op unless sharded
 void dom_allreduce(const Domain& d, double* buf, int count, int op, cudaStream_t st);
+// sharded: the whole lattice vector on every rank from the ranks' slabs (zero-padded
+// all-reduce sum: every site has exactly one nonzero contribution, so the result is exact)
+void dom_gather_full(const Domain& d, double* full, const double* part, cudaStream_t st);
 // y = (A - sig I) x on the domain (halo exchange overlapped with the interior planes)
 void dom_spmv(const Domain& d, double* y, const double* x, const double* eps, double hop, double sig,
               cudaStream_t st);

@@ -893,6 +893,226 @@ __global__ void __launch_bounds__(TB)
   }
 }
 
+// ---- staged apply (DESIGN.md sect. 4) -------------------------------------------------
+// The rows a CTA owns are consecutive, so their factor entries are ONE contiguous stream
+// [ptr[row0], ptr[row1]) of indices and values.  One thread streams it into shared memory
+// with 1-D bulk copies (cp.async.bulk, completion on an mbarrier) -- issued before
+// griddepcontrol.wait, so they overlap the previous level's tail -- in chunks of SCAP
+// entries through a ring of `nst` stages; the threads hold no prefetch registers and only
+// issue the gathers of the predecessor's output (PREF per batch).  The bulk copies cover
+// the 4-entry-aligned hull of the range (16-byte granules) and never read past the last
+// full granule of the array; the few entries beyond it come from global memory.
+constexpr int SCAP = 1920;  // entries per stage: 7.5 KB indices + 15 KB fp64 values (2 stages < 48 KB)
+
+template <typename TV>
+struct StageBuf {
+  int32_t col[SCAP];
+  TV val[SCAP];
+};
+
+template <typename TV>
+__device__ __forceinline__ void stage_issue(StageBuf<TV>* sb, const int32_t* col, const TV* val, int64_t cs,
+                                            int64_t ce, uint64_t* bar) {
+  const uint32_t n = (uint32_t)(ce - cs);
+  mbar_expect_tx(bar, n * (uint32_t)(4 + sizeof(TV)));
+  bulk_g2s(sb->col, col + cs, n * 4u, bar);
+  bulk_g2s(sb->val, val + cs, n * (uint32_t)sizeof(TV), bar);
+}
+
+// sum over this lane's entries e = e0 + lane + m G inside [lo, hi) of val[e] src[col[e]],
+// read from the stage holding entries [cs, cs + SCAP), in batches of PREF gathers
+template <int G, typename TV>
+__device__ __forceinline__ double stage_gather(int64_t e0, int lane, int64_t lo, int64_t hi, const StageBuf<TV>* b,
+                                               int64_t cs, const double* __restrict__ src) {
+  int64_t e = e0 + lane;
+  if (e < lo) e += ((lo - e + G - 1) / G) * G;
+  double acc = 0.0;
+  for (; e < hi; e += (int64_t)PREF * G) {
+    int32_t c[PREF];
+    double v[PREF];
+#pragma unroll
+    for (int q = 0; q < PREF; ++q) {
+      const int64_t ee = e + (int64_t)q * G;
+      c[q] = (ee < hi) ? b->col[ee - cs] : -1;
+      v[q] = (ee < hi) ? (double)b->val[ee - cs] : 0.0;
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < PREF; ++q)
+      if (c[q] >= 0) part += v[q] * __ldg(&src[c[q]]);
+    acc += part;
+  }
+  return acc;
+}
+
+// The CTA-wide part shared by both substitutions: stream [E0, E1) through the stages and
+// return this lane's partial sum of its row [e0, e1) (act: the thread has a row).
+// Call with the first min(nch, nst) chunks already issued (issue_first) before pdl_wait.
+template <typename TV>
+struct StagePlan {
+  int64_t SB, SE;
+  int nch;
+};
+template <typename TV>
+__device__ __forceinline__ StagePlan<TV> stage_plan(int64_t E0, int64_t E1, int64_t nnz) {
+  StagePlan<TV> p;
+  p.SB = E0 & ~int64_t(3);
+  const int64_t top = nnz & ~int64_t(3);
+  p.SE = min((E1 + 3) & ~int64_t(3), top);
+  p.nch = p.SE > p.SB ? (int)((p.SE - p.SB + SCAP - 1) / SCAP) : 0;
+  return p;
+}
+template <typename TV>
+__device__ __forceinline__ void stage_issue_first(const StagePlan<TV>& p, StageBuf<TV>* sb, uint64_t* bar, int nst,
+                                                  const int32_t* col, const TV* val) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int c = 0; c < min(p.nch, nst); ++c)
+      stage_issue(sb + c, col, val, p.SB + (int64_t)c * SCAP, min(p.SE, p.SB + (int64_t)(c + 1) * SCAP), &bar[c]);
+  }
+  __syncthreads();
+}
+template <int G, typename TV>
+__device__ __forceinline__ double stage_consume(const StagePlan<TV>& p, StageBuf<TV>* sb, uint64_t* bar, int nst,
+                                                const int32_t* __restrict__ col, const TV* __restrict__ val,
+                                                bool act, int64_t e0, int64_t e1, int lane,
+                                                const double* __restrict__ src) {
+  double acc = 0.0;
+  for (int ch = 0; ch < p.nch; ++ch) {
+    const int s = ch % nst;
+    const int64_t cs = p.SB + (int64_t)ch * SCAP, ce = min(p.SE, cs + SCAP);
+    mbar_wait(&bar[s], (uint32_t)((ch / nst) & 1));
+    if (act) acc += stage_gather<G, TV>(e0, lane, max(e0, cs), min(e1, ce), sb + s, cs, src);
+    if (ch + nst < p.nch) {
+      __syncthreads();  // every thread is done with stage s
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        stage_issue(sb + s, col, val, p.SB + (int64_t)(ch + nst) * SCAP,
+                    min(p.SE, p.SB + (int64_t)(ch + nst + 1) * SCAP), &bar[s]);
+      }
+    }
+  }
+  // entries past the last full 16-byte granule of the array (only the last CTA has them)
+  if (act && e1 > p.SE) {
+    int64_t e = e0 + lane;
+    if (e < p.SE) e += ((p.SE - e + G - 1) / G) * G;
+    for (; e < e1; e += G) acc += (double)val[e] * __ldg(&src[col[e]]);
+  }
+  return acc;
+}
+
+template <int G, typename TV>
+__global__ void __launch_bounds__(TB, 6)
+    k_apply_fwd_s(int nC, int nst, int64_t nnz, const int32_t* __restrict__ cidx, const double* __restrict__ D,
+                  const double* __restrict__ r, const double* __restrict__ gsrc, const int64_t* __restrict__ Lptr,
+                  const int32_t* __restrict__ Lcol, const TV* __restrict__ Lval, double* __restrict__ rn,
+                  double* __restrict__ rFn, const int32_t* __restrict__ fmapn) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  StageBuf<TV>* sb = reinterpret_cast<StageBuf<TV>*>(smraw);
+  __shared__ __align__(8) uint64_t bar[2];
+  pdl_launch_dependents();
+  constexpr int R = TB / G;
+  const int row0 = blockIdx.x * R, row1 = min(nC, row0 + R);
+  const int cp = row0 + threadIdx.x / G, lane = threadIdx.x % G;
+  const bool act = cp < nC;
+  const StagePlan<TV> pl = stage_plan<TV>(Lptr[row0], Lptr[row1], nnz);
+  stage_issue_first(pl, sb, bar, nst, Lcol, Lval);
+  int64_t e0 = 0, e1 = 0;
+  int c = 0, fn = -1;
+  double Dc = 0.0;
+  if (act) {
+    e0 = Lptr[cp];
+    e1 = Lptr[cp + 1];
+    c = cidx[cp];
+    Dc = D[c];
+    if (rFn && lane == 0) fn = fmapn[cp];
+  }
+  pdl_wait();
+  double acc = stage_consume<G, TV>(pl, sb, bar, nst, Lcol, Lval, act, e0, e1, lane, gsrc);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (act && lane == 0) {
+    const double v = Dc * r[c] - acc;
+    rn[cp] = v;
+    if (fn >= 0) rFn[fn] = v;
+  }
+}
+
+template <int G, typename TV>
+__global__ void __launch_bounds__(TB, 6)
+    k_apply_bwd_s(int nF, int nC, int bF, int nst, int64_t nnz, const int32_t* __restrict__ fidx,
+                  const int32_t* __restrict__ cidx, const double* __restrict__ D, const double* __restrict__ r,
+                  const int32_t* __restrict__ partner, const double* __restrict__ b11, const double* __restrict__ b12,
+                  const int64_t* __restrict__ LTptr, const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval,
+                  const double* __restrict__ zn, double* __restrict__ z, const int64_t* __restrict__ Vptr,
+                  const int32_t* __restrict__ Vcol, const double* __restrict__ Vval, const double* __restrict__ rF) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  StageBuf<TV>* sb = reinterpret_cast<StageBuf<TV>*>(smraw);
+  __shared__ __align__(8) uint64_t bar[2];
+  pdl_launch_dependents();
+  if ((int)blockIdx.x >= bF) {  // coarse part: z_c = D_c zn_c'
+    const int cp = (blockIdx.x - bF) * TB + threadIdx.x;
+    int i = 0;
+    double Di = 0.0;
+    if (cp < nC) {
+      i = cidx[cp];
+      Di = D[i];
+    }
+    pdl_wait();
+    if (cp < nC) z[i] = Di * zn[cp];
+    return;
+  }
+  constexpr int R = (TB / G) > 0 ? TB / G : 1;
+  const int row0 = blockIdx.x * R, row1 = min(nF, row0 + R);
+  const int fp = row0 + threadIdx.x / G, lane = threadIdx.x % G;
+  const bool act = fp < nF;
+  const StagePlan<TV> pl = stage_plan<TV>(LTptr[row0], LTptr[row1], nnz);
+  stage_issue_first(pl, sb, bar, nst, LTcol, LTval);
+  int64_t e0 = 0, e1 = 0;
+  int i = 0, p = -1, iv = 0;
+  double Di = 0.0, Dp = 0.0, B1 = 0.0, B2 = 0.0;
+  if (act) {
+    e0 = LTptr[fp];
+    e1 = LTptr[fp + 1];
+    if (Vptr) iv = fidx[fp];
+    if (lane == 0) {
+      i = fidx[fp];
+      Di = D[i];
+      B1 = b11[i];
+      p = partner[i];
+      if (p >= 0) {
+        Dp = D[p];
+        B2 = b12[i];
+      }
+    }
+  }
+  pdl_wait();
+  double acc = stage_consume<G, TV>(pl, sb, bar, nst, LTcol, LTval, act, e0, e1, lane, zn);
+  if (act && Vptr)  // virtual couplings: -(B~^{-1} - B_d^{-1}) r^_F  (reading R17)
+    for (int64_t e = Vptr[iv] + lane; e < Vptr[iv + 1]; e += G) {
+      const int32_t v = Vcol[e];
+      acc -= Vval[e] * (D[v] * r[v]);
+    }
+#pragma unroll
+  for (int o = (G < 32 ? G : 32) / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if constexpr (G > 32) {  // long rows (deep levels): G / 32 warps per row, fixed-order sum
+    __shared__ double part[TB / 32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (lane == 0) {
+      acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < G / 32; ++k) acc += part[(threadIdx.x >> 5) + k];
+    }
+  }
+  if (act && lane == 0) {
+    double y = B1 * (Di * (rF ? rF[fp] : r[i]));
+    if (p >= 0) y += B2 * (Dp * r[p]);
+    z[i] = Di * (y - acc);
+  }
+}
+
 // G lanes per row such that each lane holds ~per_lane entries: 8 on large levels
 // (streaming, more loads in flight per thread), 4 on small L2-resident ones (more
 // threads); measured at L = 50..200 (DESIGN.md sect. 4)
@@ -905,11 +1125,11 @@ static int pick_group(double avg_len, int64_t nnz, int gmax = 32) {
 }
 
 template <typename K, typename... Args>
-static void launch_pdl(K kernel, int grid, cudaStream_t st, Args... args) {
+static void launch_pdl_smem(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TB);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -919,10 +1139,35 @@ static void launch_pdl(K kernel, int grid, cudaStream_t st, Args... args) {
   AJ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
   AJ_LAUNCHED();
 }
+template <typename K, typename... Args>
+static void launch_pdl(K kernel, int grid, cudaStream_t st, Args... args) {
+  launch_pdl_smem(kernel, grid, 0, st, args...);
+}
+
+// stages of the staged kernels for a level (0: the register-prefetch kernels): one stage
+// when the CTAs' streams mostly fit in SCAP entries, else two (chunk c+1 in flight while c is
+// gathered).  Opt-in (AJ_APPLY_STAGED=1): measured slower than the register-prefetch kernels
+// (apply L=150 3.23 vs 2.83 ms, L=200 8.27 vs 7.43 ms; DESIGN.md sect. 4).
+static int pick_stages(int64_t nnz, int64_t rows, int g) {
+  if (!getenv("AJ_APPLY_STAGED") || rows <= 0 || nnz <= 0) return 0;
+  const double per_cta = (double)nnz / (double)ceil_div(rows, std::max(1, TB / g));
+  return per_cta <= 0.75 * SCAP ? 1 : 2;
+}
 
 template <int G>
 static void fwd_g(const Level& v, const double* r, const double* gsrc, double* rn, double* rFn,
                   const int32_t* fmapn, int grid, cudaStream_t st) {
+  if (v.nst_f > 0) {
+    if (v.f32)
+      launch_pdl_smem(k_apply_fwd_s<G, float>, grid, v.nst_f * sizeof(StageBuf<float>), st, v.nC, v.nst_f, v.nnzL,
+                      (const int32_t*)v.cidx, (const double*)v.D, r, gsrc, (const int64_t*)v.Lptr,
+                      (const int32_t*)v.Lcol, (const float*)v.Lval, rn, rFn, fmapn);
+    else
+      launch_pdl_smem(k_apply_fwd_s<G, double>, grid, v.nst_f * sizeof(StageBuf<double>), st, v.nC, v.nst_f,
+                      v.nnzL, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc, (const int64_t*)v.Lptr,
+                      (const int32_t*)v.Lcol, (const double*)v.Lval, rn, rFn, fmapn);
+    return;
+  }
   if (v.f32)
     launch_pdl(k_apply_fwd<G, float>, grid, st, v.nC, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc,
                (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const float*)v.Lval, rn, rFn, fmapn);
@@ -932,6 +1177,21 @@ static void fwd_g(const Level& v, const double* r, const double* gsrc, double* r
 }
 template <int G>
 static void bwd_g(const Level& v, const double* r, const double* zn, double* z, int bF, int grid, cudaStream_t st) {
+  if (v.nst_b > 0) {
+    if (v.f32)
+      launch_pdl_smem(k_apply_bwd_s<G, float>, grid, v.nst_b * sizeof(StageBuf<float>), st, v.nF, v.nC, bF, v.nst_b,
+                      v.nnzLT, (const int32_t*)v.fidx, (const int32_t*)v.cidx, (const double*)v.D, r,
+                      (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
+                      (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z,
+                      (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval, (const double*)v.rF);
+    else
+      launch_pdl_smem(k_apply_bwd_s<G, double>, grid, v.nst_b * sizeof(StageBuf<double>), st, v.nF, v.nC, bF,
+                      v.nst_b, v.nnzLT, (const int32_t*)v.fidx, (const int32_t*)v.cidx, (const double*)v.D, r,
+                      (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
+                      (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z,
+                      (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval, (const double*)v.rF);
+    return;
+  }
   if (v.f32)
     launch_pdl(k_apply_bwd<G, float>, grid, st, v.nF, v.nC, bF, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
@@ -1410,6 +1670,8 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
       // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
       lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0, lv.nnzLT, lv.nF <= 2048 ? TB : 32);
       if (const char* fg = getenv("AJ_FORCE_GB")) lv.gb = atoi(fg);    // testing: every backward group size
+      lv.nst_f = pick_stages(lv.nnzL, lv.nC, lv.gf);
+      lv.nst_b = pick_stages(lv.nnzLT, lv.nF, lv.gb);
       K->lv.push_back(lv);
       A.release(st);
       A = S;

@@ -44,6 +44,7 @@ struct Level {
   double* Vval = nullptr;       // b'_uv
   int64_t nnzV = 0;
   int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
+  int nst_f = 0, nst_b = 0;     // shared-memory stages of the staged kernels (0: register prefetch)
   double* rF = nullptr;         // nF: r on the pivots, compact (levels >= 1; written by the previous forward step)
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;

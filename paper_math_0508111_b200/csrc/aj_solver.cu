@@ -408,6 +408,16 @@ void Workspace::release(cudaStream_t st) {
   for (int i = 0; i < 9; ++i) dfree(vec[i], st);
 }
 
+void dom_precond(const Domain& dom, const Precond* K, double* z, const double* r, cudaStream_t st) {
+  if (!dom.sharded() || !dom.rfull) {
+    precond_run(K, z, r, st);
+    return;
+  }
+  dom_gather_full(dom, dom.rfull, r, st);
+  precond_run(K, dom.zfull, dom.rfull, st);
+  AJ_CUDA(cudaMemcpyAsync(z, dom.zfull + dom.site0(), (size_t)dom.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
 // SQMR on the projected operator.  Qt/Y: n x (m+1); column m of Qt holds q, column m of Y holds w.
 // b: right-hand side (already orthogonal to Q~); x: solution out.
 SqmrResult sqmr_run(const Precond* K, const double* eps, const Domain& dom, double hop, double shift, const double* Qt,
@@ -448,7 +458,7 @@ SqmrResult sqmr_run(const Precond* K, const double* eps, const Domain& dom, doub
   auto precond_proj = [&](int step, cudaStream_t s2) {
     // w = K^{-1} r ; q = (w - Y Hinv Q~^T w) + beta q ; rho
     if (K)
-      precond_run(K, w, r, s2);
+      dom_precond(dom, K, w, r, s2);
     else
       launch_copy(w, r, n, s2);
     if (m > 0) {

@@ -25,6 +25,10 @@ struct SqmrResult {
   bool breakdown = false;
 };
 
+// z = K^{-1} r on this rank's part: the local apply, or (sharded, replicated
+// preconditioner: dom.rfull set) all-gather r, apply the whole-lattice K, keep the slab
+void dom_precond(const Domain& dom, const Precond* K, double* z, const double* r, cudaStream_t st);
+
 SqmrResult sqmr_run(const Precond* K, const double* eps, const Domain& dom, double hop, double shift, const double* Qt,
                     const double* Y, int m, const double* Hinv, const double* b, double* x, double tol,
                     int maxit, Workspace& ws, cudaStream_t st);

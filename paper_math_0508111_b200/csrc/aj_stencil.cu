@@ -205,31 +205,6 @@ constexpr int TMA_THREADS = 256;
 constexpr int TMA_SMEM = 110 * 1024;  // two CTAs per SM
 constexpr int TMA_MP = 6;             // pairs per thread and plane: (ty+2) L <= TMA_SMEM / (8 NS)
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 struct TmaGeom {
   int T, Z, kchunk, ty_max;
 };
@@ -272,18 +247,26 @@ __global__ void __launch_bounds__(TMA_THREADS, 2)
       for (int q = 0; q < min(TMA_NS, nq); ++q) issue(q);
     const int half = L >> 1;
     const int npairs = ny * half;  // <= TMA_MP * TMA_THREADS (stage budget, tma_geom)
+    // per-thread pair offsets, the same on every plane: centre / left / right in the stage,
+    // global offset inside the band (no integer division in the plane loop)
+    int oc[TMA_MP], ol[TMA_MP], orr[TMA_MP], og[TMA_MP];
+#pragma unroll
+    for (int m = 0; m < TMA_MP; ++m) {
+      const int p = threadIdx.x + m * TMA_THREADS;
+      const int r = p < npairs ? p / half : 0;
+      const int i = p < npairs ? (p - r * half) * 2 : 0;
+      oc[m] = (r + 1) * rowlen + i;
+      ol[m] = (r + 1) * rowlen + (i == 0 ? L - 1 : i - 1);
+      orr[m] = (r + 1) * rowlen + (i + 2 == L ? 0 : i + 2);
+      og[m] = p < npairs ? r * L + i : -1;
+    }
     // eps of the next plane is loaded one plane ahead into registers (the stage holds x only)
     double2 en[TMA_MP];
     auto load_eps = [&](int k) {
-      const int64_t base = (int64_t)k * P + (int64_t)j0 * L;
+      const double* eb = eps + (int64_t)k * P + (int64_t)j0 * L;
 #pragma unroll
-      for (int m = 0; m < TMA_MP; ++m) {
-        const int p = threadIdx.x + m * TMA_THREADS;
-        if (p < npairs) {
-          const int r = p / half;
-          en[m] = __ldcs(reinterpret_cast<const double2*>(eps + base + (int64_t)r * L + (p - r * half) * 2));
-        }
-      }
+      for (int m = 0; m < TMA_MP; ++m)
+        if (og[m] >= 0) en[m] = __ldcs(reinterpret_cast<const double2*>(eb + og[m]));
     };
     load_eps(k0);
     for (int k = k0; k < k1; ++k) {
@@ -303,19 +286,16 @@ __global__ void __launch_bounds__(TMA_THREADS, 2)
       const int64_t base = (int64_t)k * P + (int64_t)j0 * L;
 #pragma unroll
       for (int m = 0; m < TMA_MP; ++m) {
-        const int p = threadIdx.x + m * TMA_THREADS;
-        if (p >= npairs) break;
-        const int r = p / half;
-        const int i = (p - r * half) * 2;
-        const int o = (r + 1) * rowlen + i;  // centre pair in the stage
+        if (og[m] < 0) break;
+        const int o = oc[m];
         const double2 xc = *reinterpret_cast<const double2*>(sc + o);
-        const double left = sc[(r + 1) * rowlen + (i == 0 ? L - 1 : i - 1)];
-        const double right = sc[(r + 1) * rowlen + (i + 2 == L ? 0 : i + 2)];
+        const double left = sc[ol[m]];
+        const double right = sc[orr[m]];
         const double2 xr0 = *reinterpret_cast<const double2*>(sc + o - rowlen);
         const double2 xr1 = *reinterpret_cast<const double2*>(sc + o + rowlen);
         const double2 xm = *reinterpret_cast<const double2*>(sm + o);
         const double2 xp = *reinterpret_cast<const double2*>(sp + o);
-        const int64_t gi = base + (int64_t)r * L + i;
+        const int64_t gi = base + og[m];
         const double s0 = (left + xc.y) + (xr0.x + xr1.x) + (xm.x + xp.x);
         const double s1 = (xc.x + right) + (xr0.y + xr1.y) + (xm.y + xp.y);
         double2 v;
@@ -340,9 +320,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 2)
   if constexpr (NV > 0) block_reduce_finalize<NV, TMA_THREADS>(acc, rb, blockIdx.x, gridDim.x);
 }
 
-// Kernel choice for the full-lattice SpMV.  Default: the balanced one-wave z-march for
-// even L >= 64 (measured at L=250: see DESIGN.md sect. 4), the tiled z-march otherwise.
-// AJ_SPMV_PATH=tma|bal|grid (testing) forces one (tma/bal need even L, tma 64 <= L <= 512).
+// Kernel choice for the full-lattice SpMV (measured at L=100..250, DESIGN.md sect. 4):
+// the TMA-staged kernel for the plain product (nv = 0) at even 128 <= L <= 512, the tiled
+// register z-march otherwise (with fused dots the extra dot-vector streams keep enough
+// loads in flight: 5.0 TB/s at L=250).  AJ_SPMV_PATH=tma|bal|grid (testing) forces one
+// (tma/bal need even L, tma 64 <= L <= 512).
 enum SpmvPath { SP_GRID1, SP_GRID2, SP_BAL, SP_TMA };
 
 static TmaGeom tma_geom(int L) {
@@ -360,13 +342,13 @@ static TmaGeom tma_geom(int L) {
   return g;
 }
 
-static SpmvPath spmv_path(int L) {
+static SpmvPath spmv_path(int L, int nv) {
   if (L % 2 != 0) return SP_GRID1;
   const char* e = getenv("AJ_SPMV_PATH");
   if (e && !strcmp(e, "tma") && tma_geom(L).T > 0) return SP_TMA;
   if (e && !strcmp(e, "grid")) return SP_GRID2;
   if (e && !strcmp(e, "bal")) return SP_BAL;
-  return L >= 64 ? SP_BAL : SP_GRID2;
+  return (nv == 0 && L >= 128 && tma_geom(L).T > 0) ? SP_TMA : SP_GRID2;
 }
 
 static size_t tma_smem_bytes(const TmaGeom& g, int L) { return (size_t)TMA_NS * (g.ty_max + 2) * L * 8; }
@@ -427,13 +409,13 @@ static void spmv_dispatch(SpmvPath path, double* y, const double* x, const doubl
 void launch_spmv(double* y, const double* x, const double* eps, int L, double hop, double sig,
                  cudaStream_t st) {
   ProfScope ps(PROF_SPMV, 24.0 * L * L * L, st);
-  spmv_dispatch<0>(spmv_path(L), y, x, eps, L, hop, sig, nullptr, 0, RedBuf{}, st);
+  spmv_dispatch<0>(spmv_path(L, 0), y, x, eps, L, hop, sig, nullptr, 0, RedBuf{}, st);
 }
 
 void launch_spmv_dots(double* y, const double* x, const double* eps, int L, double hop, double sig,
                       const double* W, int64_t ld, int nv, const RedBuf& rb, cudaStream_t st) {
   ProfScope ps(PROF_SPMV, (24.0 + 8.0 * nv) * L * L * L, st);
-  const SpmvPath path = spmv_path(L);
+  const SpmvPath path = spmv_path(L, nv);
   switch (nv) {
 #define CASE(N)                                                       \
   case N:                                                             \
@@ -588,6 +570,14 @@ void dom_allreduce(const Domain& d, double* buf, int count, int op, cudaStream_t
   if (!d.sharded() || count <= 0) return;
   const int rc = d.comm->allreduce(d.comm->ctx, buf, count, op, (void*)st);
   AJ_REQUIRE(rc == 0, AJ_ERR_CUDA, "comm allreduce failed (code " + std::to_string(rc) + ")");
+}
+
+void dom_gather_full(const Domain& d, double* full, const double* part, cudaStream_t st) {
+  const int64_t N = (int64_t)d.L * d.L * d.L;
+  AJ_REQUIRE(N < (int64_t)INT32_MAX, AJ_ERR_ARG, "dom_gather_full: L^3 exceeds the comm's int32 count");
+  AJ_CUDA(cudaMemsetAsync(full, 0, (size_t)N * sizeof(double), st));
+  AJ_CUDA(cudaMemcpyAsync(full + d.site0(), part, (size_t)d.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (d.sharded()) dom_allreduce(d, full, (int)N, 0, st);
 }
 
 // interior planes [1, nz-1) while the halo planes travel, then planes 0 and nz-1

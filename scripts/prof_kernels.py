@@ -37,7 +37,11 @@ def main():
             ms = e0.elapsed_time(e1) / reps
             print(f"spmv[{path}] L={L}: {ms:.4f} ms  {24 * n / ms / 1e6:.1f} GB/s", flush=True)
         os.environ.pop("AJ_SPMV_PATH", None)
-    if what in ("precond", "all"):
+    if what in ("precond", "all", "precond2"):
+      for mode in (("register", "staged") if what == "precond2" else ("default",)):
+        if mode == "staged":
+            os.environ["AJ_APPLY_STAGED"] = "1"
+        print(f"-- apply kernels: {mode}", flush=True)
         t0 = time.perf_counter()
         K = binding.Precond(eps, L, -1.0, 0.0)
         torch.cuda.synchronize()

@@ -33,22 +33,34 @@ def main():
     if "AJ_INNER_TOL" in os.environ:
         jp.inner_tol = float(os.environ["AJ_INNER_TOL"])
     pp = binding.default_precond_params()
-    for key, env in (("tau_drop", "AJ_TD"), ("tau_strong", "AJ_TS"), ("tau_virtual", "AJ_TV")):
+    for key, env in (("tau_drop", "AJ_TD"), ("tau_strong", "AJ_TS"), ("tau_virtual", "AJ_TV"), ("tau_inv", "AJ_TINV"),
+                     ("kappa", "AJ_KAPPA")):
         if env in os.environ:
             setattr(pp, key, float(os.environ[env]))
     if "AJ_DENSE_CAP" in os.environ:
         pp.dense_cap = int(os.environ["AJ_DENSE_CAP"])
+    if "AJ_NCOARSE" in os.environ:
+        pp.n_coarse_max = int(os.environ["AJ_NCOARSE"])
     t0 = time.perf_counter()
-    lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp, jparams=jp)
+    try:
+        lam, X, res, st = binding.jd_solve(cfg["k"], cfg["sigma"], cfg["tol"], eps, L, cfg["hop"], pparams=pp,
+                                           jparams=jp)
+    except Exception as ex:  # report the failure as a JSON line too
+        print(json.dumps(dict(config=c, L=L, W=cfg["W"], seed=cfg["seed"], error=str(ex)[:300],
+                              wall_s=time.perf_counter() - t0, env={k: v for k, v in os.environ.items()
+                                                                    if k.startswith("AJ_")})), flush=True)
+        return
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     normA = 6 * abs(cfg["hop"]) + float(eps.abs().max())
     G = (X.T @ X).cpu().numpy()
-    out = dict(config=c, L=L, W=cfg["W"], seed=cfg["seed"], wall_s=dt, setup_ms=st["setup_ms"],
+    out = dict(config=c, L=L, W=cfg["W"], seed=cfg["seed"], wall_s=dt,
+               env={k: v for k, v in os.environ.items() if k.startswith("AJ_")}, setup_ms=st["setup_ms"],
                solve_ms=st["solve_ms"], outer=st["outer"], inner=st["inner_total"],
                levels=st["precond"]["levels"], coarse=st["precond"]["coarse_n"],
                tau_drop=st["precond"]["tau_drop"], tau_strong=st["precond"]["tau_strong"],
                tau_virtual=st["precond"]["tau_virtual"], nnz_V=st["precond"]["nnz_V"],
+               tau_inv=st["precond"]["tau_inv"], nnz_L_dropped_inv=st["precond"]["nnz_L_dropped_inv"],
                nnzL_per_site=st["precond"]["nnz_L"] / L ** 3, eigenvalues=[float(v) for v in lam],
                resid_rel=[float(v) / normA for v in res], orth_err=float(np.abs(G - np.eye(len(lam))).max()))
     print(json.dumps(out), flush=True)

@@ -2,7 +2,7 @@
 same seeded inputs.  Tolerances (DESIGN.md sect. 5):
   disorder      bit-exact (integer hash -> exact double arithmetic)
   spmv          max|y - y_ref| <= 1e-14 * max|y_ref|          (BASELINE north_star)
-  precond       same level structure; ||z - z_ref|| <= 1e-8 ||z_ref||
+  precond       same level structure; ||z - z_ref|| <= 1e-12 ||z_ref|| (APPLY_TOL)
   sqmr          converged to tol, true residual <= 10 tol
   multi_dot     <= 1e-13 relative
   jd_solve      |lambda - lambda_ref| <= 1e-10 ||A||, ||Ax - lambda x|| <= 1e-8 ||A||,
@@ -24,8 +24,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 # preconditioner apply parity, relative 2-norm; the factor is the oracle's entry for entry,
-# so the difference is the summation order of the gathers (DESIGN.md sect. 5)
-APPLY_TOL = 1e-8
+# so the difference is the summation order of the gathers (DESIGN.md sect. 5).  Observed on
+# the B200 (round 2, AJ_PARITY_LOG): median 1.3e-14, max 9.5e-14 over every case except the
+# uncompensated W=21 L=11 factor (1.36e-12, a more ill-conditioned coarse inverse) -> ~10x.
+APPLY_TOL = 1e-12
+APPLY_TOL_ILLCOND = 1e-11
 
 
 def _log_parity(name, case, err):
@@ -202,7 +205,7 @@ def test_precond_parity(gpu_lib, L, W, seed, hop, sigma, fp32, comp):
         zr = M.apply(r)
         err = np.linalg.norm(N(z) - zr) / np.linalg.norm(zr)
         _log_parity("precond", (L, W, seed, fp32, comp), err)
-        assert err <= APPLY_TOL, err
+        assert err <= (APPLY_TOL_ILLCOND if (W, comp) == (21.0, 0) else APPLY_TOL), err
     K.free()
 
 
@@ -244,11 +247,13 @@ def oracle_l48(gpu_lib):
 
 @pytest.mark.parametrize("variant", [{}, {"AJ_PER_LANE": "8"}, {"AJ_PER_LANE": "2"}, {"AJ_SCHUR_TIER": "2"},
                                      {"AJ_SCHUR_TIER": "3"}, {"AJ_SCHUR_TIER": "4"}, {"AJ_SCHUR_TIER": "5"},
-                                     {"AJ_FORCE_GB": "64"}, {"AJ_FORCE_GB": "256"}, {"AJ_GJ_STEPS": "1"}])
+                                     {"AJ_FORCE_GB": "64"}, {"AJ_FORCE_GB": "256"}, {"AJ_GJ_STEPS": "1"},
+                                     {"AJ_APPLY_STAGED": "1"}, {"AJ_APPLY_STAGED": "1", "AJ_FORCE_GB": "128"}])
 def test_precond_parity_production_l48(gpu_lib, monkeypatch, oracle_l48, variant):
     # GPU vs ORACLE at a size spanning many tiles (24 levels, coarse ~900) with the production
     # parameters, once with the routed default and once with each kernel variant forced
-    # (row-group lanes, every Schur tier, CTA-per-row backward, the swap-based coarse inverse)
+    # (row-group lanes, every Schur tier, CTA-per-row backward, the swap-based coarse inverse,
+    # the bulk-copy staged substitution kernels)
     import torch
     o = oracle_l48
     for k, v in variant.items():
@@ -495,6 +500,34 @@ def test_jd_config1_l50(gpu_lib):
     for i in range(k):
         r = an.stencil_apply(L, e, Xh[:, i], hop=hop) - lam[i] * Xh[:, i]
         assert np.linalg.norm(r) <= 1e-8 * normA
+
+
+def test_jd_config1_l50_subspace_angles(gpu_lib):
+    # configs[1] eigenVECTORS against the oracle golden (tests/golden/eigvecs_config1.npz,
+    # plain SI-Lanczos, residuals ~1e-14): the north star's angle bound 1e-7.  Davis-Kahan:
+    # angle_i <= ||r_i|| / gap_i; with gaps ~4e-5 near E=0 at L=50 the solve runs to
+    # tol 2e-13 (||r|| <= 2.9e-12) so that the bound certifies 1e-7.
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "eigs_config1.json")))
+    Xg = np.load(os.path.join(ROOT, "tests", "golden", gold["eigenvectors"]))["X"]   # (k, n)
+    cfg = CONFIGS[1]
+    L, W, seed, hop, k = cfg["L"], cfg["W"], cfg["seed"], cfg["hop"], cfg["k"]
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, 2e-13, eps, L, hop)
+    Xh = N(X)
+    lg = np.array(gold["eigenvalues"])          # the k + 3 nearest sigma = 0, ascending |lambda|
+    normA = 6 + np.abs(an.disorder(L, W, seed)).max()
+    assert np.all(np.abs(np.sort(lam) - np.sort(lg[:k])) <= 1e-10 * normA)
+    for i in range(k):
+        j = int(np.argmin(np.abs(lg[:k] - lam[i])))
+        gap = np.min(np.abs(np.delete(lg, j) - lg[j]))
+        # angle via the chordal distance 2 sin(angle/2) of the unit vectors (arccos of the
+        # cosine loses all digits below ~1e-8)
+        sgn = 1.0 if float(Xh[:, i] @ Xg[j]) >= 0 else -1.0
+        ang = 2 * np.arcsin(min(1.0, np.linalg.norm(Xh[:, i] / np.linalg.norm(Xh[:, i]) - sgn * Xg[j]) / 2))
+        bound = res[i] / gap
+        assert bound <= 1e-7, (i, bound)            # the certificate itself
+        assert ang <= 1e-7, (i, ang, bound)
+        assert ang <= 2 * bound + 1e-9, (i, ang, bound)
 
 
 def test_jd_host_e2e(gpu_lib):

@@ -161,6 +161,14 @@ def log(*a):
     print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
+def resolved_drop(L, kappa=5.0):
+    """The library's auto drop parameters (aj_mlildl.cu resolve_params): tau_drop = the
+    paper's eps/kappa, eps = 1/sqrt(L^3); tau_strong = min(0.05, 40 tau_drop); tau_virtual =
+    5..10 tau_drop for L = 50..100."""
+    td = 1.0 / (kappa * (float(L) ** 1.5))
+    return td, min(0.05, 40.0 * td), min(10.0, max(5.0, 5.0 + 5.0 * (L - 50) / 50.0)) * td
+
+
 def _oracle_solve(job):
     """One full oracle solve (multilevel ILDL setup + JD, oracle/mlildl.py + oracle/jd.py,
     numpy/scipy on 1 thread) of the workload `cfg`; returns (seconds, eigenvalues)."""
@@ -177,7 +185,9 @@ def _oracle_solve(job):
         t0 = time.perf_counter()
         e = an.disorder(L, W, seed)
         A = an.matrix(L, e, hop=hop)
-        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=1024)
+        td, ts, tv = resolved_drop(L)    # the GPU path's default parameters (R12, R17)
+        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=1024,
+                                  tau_drop=td, tau_strong=ts, tau_virtual=tv)
         lam, X, st = jd_nearest(A, M.apply, k, sigma=sigma, tol=tol)
         dt = time.perf_counter() - t0
     return dt, [float(v) for v in lam]
@@ -491,7 +501,8 @@ def run_ours(args, cfg, ws, rank, local):
             e1.record(st)
             e1.synchronize()
             per.append(e0.elapsed_time(e1))
-            log(f"step: {per[-1]:.1f} ms")
+            log(f"step: {per[-1]:.1f} ms (setup {stats['setup_ms']:.1f} ms, solve {stats['solve_ms']:.1f} ms, "
+                f"outer {stats['outer']}, inner {stats['inner_total']})")
         torch.cuda.synchronize()
     barrier(ws)
     torch.cuda.synchronize()

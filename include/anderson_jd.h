@@ -99,8 +99,9 @@ AJ_API int spmv_slab(double* d_y, const double* d_x_ext, const double* d_eps, in
  * ------------------------------------------------------------------------- */
 typedef struct {
   double kappa;          /* inverse bound, paper default 5    */
-  double tau_drop;       /* drop tolerance for L and S (paper: eps/kappa);
-                            < 0: auto, 2e-3 * min(1, (50/L)^2)                    */
+  double tau_drop;       /* drop tolerance for L and S; < 0: auto = the paper's
+                            eps/kappa with eps = 1/sqrt(N), N = L^3
+                            (R12)           */
   double tau_strong;     /* strong-coupling threshold of the independent sets;
                             < 0: auto, min(0.05, 40 tau_drop) with compensation,
                             else 10 * tau_drop                                    */

@@ -101,7 +101,7 @@ int spmv_slab(double* d_y, const double* d_x_ext, const double* d_eps, int32_t L
 void aj_precond_default_params(aj_precond_params* p) {
   if (!p) return;
   p->kappa = 5.0;
-  p->tau_drop = -1.0;      // auto: 2e-3 (50/L)^2 (R12)
+  p->tau_drop = -1.0;      // auto: 1/(kappa sqrt(L^3)), the paper's eps/kappa (R12)
   p->tau_strong = -1.0;    // auto: min(0.05, 40 tau_drop) (R17), 10 tau_drop without compensation
   p->n_coarse_max = 1024;
   p->max_levels = 1023;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -705,6 +706,274 @@ __global__ void __launch_bounds__(TB) k_gj_step(int n, int k, double* __restrict
   __threadfence();
   gj_pick_and_stage(n, k + 1, M, S, gridDim.x);
   if (threadIdx.x == 0) *S.count = 0u;
+}
+
+// ---- blocked Gauss-Jordan (default for the coarse inverse; DESIGN.md sect. 4) ----------
+// Panels of GB columns.  For panel [k0, k0+b): (1) the panel columns of every row are
+// copied (Pold, untouched, and Pw, the working copy); (2) b per-column steps on Pw only
+// (n x b, L2-resident) choose the pivot rows P exactly like k_gj_step (largest |a| among
+// the rows not yet pivoted, smallest row on ties) and eliminate within the panel;
+// (3) Binv = Pold[P, :]^{-1} (b x b, one CTA, partial pivoting); W = Binv M[P, c] for the
+// columns c >= k0+b still read; (4) the block Gauss-Jordan update of every row:
+// M[P_l, c] = W[l, c], M[i, c] -= Pold[i, :] W[:, c] (i not in P) -- one rank-b pass over
+// the matrix per panel instead of b passes.  Row P_k of the right half ends as row k of
+// the inverse, as with implicit pivoting (k_gj_extract_perm).
+constexpr int GB = 32;
+
+__global__ void k_pan_load(int n, const double* __restrict__ M, int k0, int b, double* __restrict__ Pold,
+                           double* __restrict__ Pw) {
+  const int64_t w = 2 * (int64_t)n;
+  for (int64_t t = blockIdx.x * (int64_t)TB + threadIdx.x; t < (int64_t)n * b; t += (int64_t)gridDim.x * TB) {
+    const int64_t i = t / b, c = t % b;
+    const double v = M[i * w + k0 + c];
+    Pold[t] = v;
+    Pw[t] = v;
+  }
+}
+
+// pick the pivot of panel column jj among the CTAs' candidates, scale and stage its row
+__device__ void pan_pick(int n, int b, int jj, int k0, double* __restrict__ Pw, GjState S, int nparts) {
+  __shared__ double rv[TB];
+  __shared__ int ri[TB];
+  __shared__ int s_p;
+  __shared__ double s_inv;
+  double bb = -1.0;
+  int bp = n;
+  for (int c = threadIdx.x; c < nparts; c += TB) {
+    const double v = __ldcg(&S.pv[c]);
+    const int ix = __ldcg(&S.pi[c]);
+    if (v > bb || (v == bb && ix < bp)) {
+      bb = v;
+      bp = ix;
+    }
+  }
+  rv[threadIdx.x] = bb;
+  ri[threadIdx.x] = bp;
+  __syncthreads();
+  for (int s2 = TB / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2 &&
+        (rv[threadIdx.x + s2] > rv[threadIdx.x] || (rv[threadIdx.x + s2] == rv[threadIdx.x] && ri[threadIdx.x + s2] < ri[threadIdx.x]))) {
+      rv[threadIdx.x] = rv[threadIdx.x + s2];
+      ri[threadIdx.x] = ri[threadIdx.x + s2];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bb = rv[0];
+    bp = ri[0];
+    if (!(bb > 0.0) || bp >= n) {
+      *S.singular = 1;
+      bp = -1;
+    } else {
+      S.prow_idx[k0 + jj] = bp;
+      S.pivoted[bp] = 1;
+      s_inv = 1.0 / __ldcg(&Pw[(int64_t)bp * b + jj]);
+    }
+    s_p = bp;
+  }
+  __syncthreads();
+  const int p = s_p;
+  if (p < 0) return;
+  double* pr = S.prow + (int64_t)(jj & 1) * GB;
+  for (int c = jj + threadIdx.x; c < b; c += TB) {
+    const double v = __ldcg(&Pw[(int64_t)p * b + c]) * s_inv;
+    Pw[(int64_t)p * b + c] = v;
+    pr[c] = v;
+  }
+}
+
+// candidates for panel column 0 (one CTA)
+__global__ void k_pan_first(int n, int b, int k0, double* __restrict__ Pw, GjState S) {
+  __shared__ double sv[TB];
+  __shared__ int si[TB];
+  double best = -1.0;
+  int bi = n;
+  for (int i = threadIdx.x; i < n; i += TB) {
+    if (S.pivoted[i]) continue;
+    const double a = fabs(Pw[(int64_t)i * b]);
+    if (a > best) {
+      best = a;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s2 = TB / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2 &&
+        (sv[threadIdx.x + s2] > sv[threadIdx.x] || (sv[threadIdx.x + s2] == sv[threadIdx.x] && si[threadIdx.x + s2] < si[threadIdx.x]))) {
+      sv[threadIdx.x] = sv[threadIdx.x + s2];
+      si[threadIdx.x] = si[threadIdx.x + s2];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S.pv[0] = sv[0];
+    S.pi[0] = si[0];
+  }
+  __threadfence_block();
+  __syncthreads();
+  pan_pick(n, b, 0, k0, Pw, S, 1);
+}
+
+// step jj of the panel: eliminate panel column jj from every row but its pivot row (panel
+// columns > jj only), propose candidates for column jj+1, the last CTA picks
+__global__ void __launch_bounds__(TB) k_pan_step(int n, int b, int jj, int k0, double* __restrict__ Pw, GjState S) {
+  __shared__ bool s_last;
+  if (*(volatile int*)S.singular) return;
+  const int p = S.prow_idx[k0 + jj];
+  const double* pr = S.prow + (int64_t)(jj & 1) * GB;
+  const bool next = jj + 1 < b;
+  // one warp per row, lanes over the panel columns
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double best = -1.0;
+  int bi = n;
+  for (int i = blockIdx.x * (TB / 32) + wid; i < n; i += gridDim.x * (TB / 32)) {
+    double* Pi = Pw + (int64_t)i * b;
+    if (i != p) {
+      const double f = Pi[jj];
+      if (f != 0.0)
+        for (int c = jj + 1 + lane; c < b; c += 32) Pi[c] -= f * pr[c];
+    }
+    __syncwarp();
+    if (lane == 0 && next && !S.pivoted[i]) {
+      const double a = fabs(Pi[jj + 1]);
+      if (a > best) {
+        best = a;
+        bi = i;
+      }
+    }
+  }
+  if (!next) return;
+  __shared__ double wv[TB / 32];
+  __shared__ int wi[TB / 32];
+  if (lane == 0) {
+    wv[wid] = best;
+    wi[wid] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < TB / 32; ++q)
+      if (wv[q] > best || (wv[q] == best && wi[q] < bi)) {
+        best = wv[q];
+        bi = wi[q];
+      }
+    S.pv[blockIdx.x] = best;
+    S.pi[blockIdx.x] = bi;
+    __threadfence();
+    s_last = atomicAdd(S.count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  pan_pick(n, b, jj + 1, k0, Pw, S, gridDim.x);
+  if (threadIdx.x == 0) *S.count = 0u;
+}
+
+// Binv = (Pold[P, :])^{-1} with partial pivoting (one CTA, b <= GB); pos[P_l] = l
+__global__ void k_pan_binv(int b, int k0, const double* __restrict__ Pold, const int* __restrict__ prow_idx,
+                           double* __restrict__ Binv, int* __restrict__ pos, int* __restrict__ singular) {
+  __shared__ double A[GB][2 * GB + 1];
+  __shared__ int s_piv;
+  for (int t = threadIdx.x; t < b * 2 * b; t += blockDim.x) {
+    const int r = t / (2 * b), c = t % (2 * b);
+    A[r][c] = (c < b) ? Pold[(int64_t)prow_idx[k0 + r] * b + c] : (c - b == r ? 1.0 : 0.0);
+  }
+  if (threadIdx.x < b) pos[prow_idx[k0 + threadIdx.x]] = threadIdx.x;
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    if (threadIdx.x == 0) {
+      int p = k;
+      for (int r = k + 1; r < b; ++r)
+        if (fabs(A[r][k]) > fabs(A[p][k])) p = r;
+      if (A[p][k] == 0.0) *singular = 1;
+      s_piv = p;
+    }
+    __syncthreads();
+    const int p = s_piv;
+    if (p != k)
+      for (int c = threadIdx.x; c < 2 * b; c += blockDim.x) {
+        const double t = A[k][c];
+        A[k][c] = A[p][c];
+        A[p][c] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / A[k][k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < 2 * b; c += blockDim.x) A[k][c] *= inv;
+    __syncthreads();
+    for (int t = threadIdx.x; t < b * 2 * b; t += blockDim.x) {
+      const int r = t / (2 * b), c = t % (2 * b);
+      if (r != k && c != k) A[r][c] -= A[r][k] * A[k][c];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < b; r += blockDim.x)
+      if (r != k) A[r][k] = 0.0;
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) Binv[t] = A[t / b][b + t % b];
+}
+
+// W[l, c - c0] = sum_m Binv[l, m] M[P_m, c], c in [c0, 2n)
+__global__ void k_pan_W(int n, int b, int k0, const double* __restrict__ M, const int* __restrict__ prow_idx,
+                        const double* __restrict__ Binv, double* __restrict__ W) {
+  __shared__ double Bs[GB * GB];
+  __shared__ int Ps[GB];
+  for (int t = threadIdx.x; t < b * b; t += TB) Bs[t] = Binv[t];
+  if (threadIdx.x < b) Ps[threadIdx.x] = prow_idx[k0 + threadIdx.x];
+  __syncthreads();
+  const int64_t w = 2 * (int64_t)n;
+  const int64_t c0 = k0 + b, R = w - c0;
+  for (int64_t c = blockIdx.x * (int64_t)TB + threadIdx.x; c < R; c += (int64_t)gridDim.x * TB) {
+    double m[GB];
+#pragma unroll
+    for (int l = 0; l < GB; ++l) m[l] = (l < b) ? M[(int64_t)Ps[l] * w + c0 + c] : 0.0;
+    for (int l = 0; l < b; ++l) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < GB; ++q) a += Bs[l * b + (q < b ? q : 0)] * (q < b ? m[q] : 0.0);
+      W[(int64_t)l * R + c] = a;
+    }
+  }
+}
+
+// the rank-b block update of rows [blockIdx.y * PR, ...) over the columns c >= k0+b
+constexpr int PR = 64;
+__global__ void __launch_bounds__(TB) k_pan_update(int n, int b, int k0, double* __restrict__ M,
+                                                   const double* __restrict__ Pold, const double* __restrict__ W,
+                                                   const int* __restrict__ pos) {
+  __shared__ double Ps[PR][GB];
+  __shared__ int ps[PR];
+  const int r0 = blockIdx.y * PR;
+  for (int t = threadIdx.x; t < PR * GB; t += TB) {
+    const int r = t / GB, l = t % GB;
+    Ps[r][l] = (r0 + r < n && l < b) ? Pold[(int64_t)(r0 + r) * b + l] : 0.0;
+  }
+  for (int r = threadIdx.x; r < PR; r += TB) ps[r] = (r0 + r < n) ? pos[r0 + r] : -1;
+  __syncthreads();
+  const int64_t w = 2 * (int64_t)n;
+  const int64_t c0 = k0 + b, R = w - c0;
+  const int rows = min(PR, n - r0);
+  for (int64_t c = blockIdx.x * (int64_t)TB + threadIdx.x; c < R; c += (int64_t)gridDim.x * TB) {
+    double wc[GB];
+#pragma unroll
+    for (int l = 0; l < GB; ++l) wc[l] = (l < b) ? W[(int64_t)l * R + c] : 0.0;
+    for (int r = 0; r < rows; ++r) {
+      double* m = M + (int64_t)(r0 + r) * w + c0 + c;
+      if (ps[r] >= 0) {
+        *m = W[(int64_t)ps[r] * R + c];  // a pivot row of this panel: the scaled block row
+      } else {
+        double a = *m;
+#pragma unroll
+        for (int l = 0; l < GB; ++l) a -= Ps[r][l] * wc[l];
+        *m = a;
+      }
+    }
+  }
+}
+
+__global__ void k_pan_clear_pos(int b, int k0, const int* __restrict__ prow_idx, int* __restrict__ pos) {
+  if (threadIdx.x < b) pos[prow_idx[k0 + threadIdx.x]] = -1;
 }
 
 // A^{-1}[k][:] = R[prow_idx[k]][:] (implicit pivoting), symmetrised
@@ -1599,8 +1868,9 @@ static double wall_ms() {
 // eps = 1/sqrt(N)).
 aj_precond_params resolve_params(const aj_precond_params& in, int L) {
   aj_precond_params P = in;
-  const double sc = (50.0 / L) * (50.0 / L);
-  if (P.tau_drop < 0.0) P.tau_drop = std::min(2e-3, 2e-3 * sc);
+  // the paper's rule: drop at eps / kappa with
+  // eps = 1/sqrt(N), N = L^3 the whole lattice (also for a z-slab shard); R12
+  if (P.tau_drop < 0.0) P.tau_drop = 1.0 / (P.kappa * std::sqrt((double)L * L * L));
   if (P.tau_strong < 0.0) P.tau_strong = P.compensate ? std::min(0.05, 40.0 * P.tau_drop) : 10.0 * P.tau_drop;
   if (P.tau_virtual < 0.0)  // 5 tau_drop up to L = 50, 10 tau_drop from L = 100 (measured, R17)
     P.tau_virtual = std::min(10.0, std::max(5.0, 5.0 + 5.0 * (L - 50) / 50.0)) * P.tau_drop;
@@ -1709,7 +1979,57 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
         AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
         k_gj_extract<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, K->G);
         AJ_LAUNCHED();
-      } else {
+      } else if (!getenv("AJ_GJ_UNBLOCKED")) {  // default: blocked Gauss-Jordan, panels of GB columns
+        const int gs = std::min(nc, num_sms() * 4);
+        GjState S;
+        S.prow_idx = dalloc<int>(nc, st);
+        S.pivoted = dalloc<int8_t>(nc, st);
+        S.prow = dalloc<double>(2 * GB, st);
+        S.pv = dalloc<double>(gs, st);
+        S.pi = dalloc<int>(gs, st);
+        S.count = dalloc<unsigned int>(1, st);
+        S.singular = sing;
+        double* Pold = dalloc<double>((int64_t)nc * GB, st);
+        double* Pw = dalloc<double>((int64_t)nc * GB, st);
+        double* Binv = dalloc<double>(GB * GB, st);
+        double* Wb = dalloc<double>((int64_t)GB * 2 * nc, st);
+        int* pos = dalloc<int>(nc, st);
+        AJ_CUDA(cudaMemsetAsync(S.pivoted, 0, nc, st));
+        AJ_CUDA(cudaMemsetAsync(S.count, 0, sizeof(unsigned int), st));
+        AJ_CUDA(cudaMemsetAsync(pos, 0xff, (size_t)nc * sizeof(int), st));
+        const int rows_ctas = std::max(1, std::min(gs, ceil_div(nc, TB / 32)));
+        for (int k0 = 0; k0 < nc; k0 += GB) {
+          const int b = std::min(GB, nc - k0);
+          k_pan_load<<<std::min(grid_for((int64_t)nc * b), num_sms() * 8), TB, 0, st>>>(nc, M, k0, b, Pold, Pw);
+          AJ_LAUNCHED();
+          k_pan_first<<<1, TB, 0, st>>>(nc, b, k0, Pw, S);
+          AJ_LAUNCHED();
+          for (int jj = 0; jj < b; ++jj) {
+            k_pan_step<<<rows_ctas, TB, 0, st>>>(nc, b, jj, k0, Pw, S);
+            AJ_LAUNCHED();
+          }
+          k_pan_binv<<<1, 256, 0, st>>>(b, k0, Pold, S.prow_idx, Binv, pos, sing);
+          AJ_LAUNCHED();
+          const int64_t R = 2 * (int64_t)nc - k0 - b;
+          if (R > 0) {
+            const int gx = std::max(1, std::min(ceil_div(R, TB), num_sms() * 4));
+            k_pan_W<<<gx, TB, 0, st>>>(nc, b, k0, M, S.prow_idx, Binv, Wb);
+            AJ_LAUNCHED();
+            const int gxu = std::max(1, std::min(ceil_div(R, TB), 64));
+            k_pan_update<<<dim3(gxu, ceil_div(nc, PR)), TB, 0, st>>>(nc, b, k0, M, Pold, Wb, pos);
+            AJ_LAUNCHED();
+          }
+          k_pan_clear_pos<<<1, GB, 0, st>>>(b, k0, S.prow_idx, pos);
+          AJ_LAUNCHED();
+        }
+        AJ_REQUIRE(read_scalar(sing, st) == 0, AJ_ERR_BREAKDOWN, "coarse Schur complement is singular");
+        k_gj_extract_perm<<<std::min(grid_for((int64_t)nc * nc), num_sms() * 16), TB, 0, st>>>(nc, M, S.prow_idx,
+                                                                                               K->G);
+        AJ_LAUNCHED();
+        for (void* q : {(void*)S.prow_idx, (void*)S.pivoted, (void*)S.prow, (void*)S.pv, (void*)S.pi, (void*)S.count,
+                        (void*)Pold, (void*)Pw, (void*)Binv, (void*)Wb, (void*)pos})
+          dfree(q, st);
+      } else {  // testing (AJ_GJ_UNBLOCKED): one launch per column
         const int gs = std::min(nc, num_sms() * (getenv("AJ_GJ_CTAS") ? atoi(getenv("AJ_GJ_CTAS")) : 4));
         GjState S;
         S.prow_idx = dalloc<int>(nc, st);

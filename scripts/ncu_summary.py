@@ -17,7 +17,8 @@ cnt = defaultdict(int)
 for r in rd:
     if r.get("Metric Name") != "gpu__time_duration.sum":
         continue
-    name = r["Kernel Name"].split("(")[0]
+    kn = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("void ", "").replace("aj::", "")
+    name = kn.split("(")[0]
     v = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "nsecond")
     scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1e-6)

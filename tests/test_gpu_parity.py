@@ -157,8 +157,9 @@ def test_spmv_plane_wave_gpu(gpu_lib):
 
 # ---------------------------------------------------------------- preconditioner
 def resolved(p, L):
-    """DESIGN.md R12 auto rule for negative drop parameters."""
-    td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
+    """DESIGN.md R12 auto rule for negative drop parameters: the paper's eps/kappa,
+    eps = 1/sqrt(N)."""
+    td = p.tau_drop if p.tau_drop >= 0 else 1.0 / (p.kappa * np.sqrt(float(L) ** 3))
     if p.tau_strong >= 0:
         ts = p.tau_strong
     else:
@@ -248,6 +249,7 @@ def oracle_l48(gpu_lib):
 @pytest.mark.parametrize("variant", [{}, {"AJ_PER_LANE": "8"}, {"AJ_PER_LANE": "2"}, {"AJ_SCHUR_TIER": "2"},
                                      {"AJ_SCHUR_TIER": "3"}, {"AJ_SCHUR_TIER": "4"}, {"AJ_SCHUR_TIER": "5"},
                                      {"AJ_FORCE_GB": "64"}, {"AJ_FORCE_GB": "256"}, {"AJ_GJ_STEPS": "1"},
+                                     {"AJ_GJ_UNBLOCKED": "1"},
                                      {"AJ_APPLY_STAGED": "1"}, {"AJ_APPLY_STAGED": "1", "AJ_FORCE_GB": "128"}])
 def test_precond_parity_production_l48(gpu_lib, monkeypatch, oracle_l48, variant):
     # GPU vs ORACLE at a size spanning many tiles (24 levels, coarse ~900) with the production
@@ -326,24 +328,51 @@ def test_precond_backward_group_sizes_agree(gpu_lib, monkeypatch):
         assert torch.linalg.norm(z - zs[None]) <= 1e-13 * torch.linalg.norm(zs[None]), gb
 
 
-def test_coarse_inverse_paths_agree(gpu_lib, monkeypatch):
-    # one-launch-per-column Gauss-Jordan with implicit pivoting (default) == the
-    # swap-based two-launch path, bit for bit (same pivots, same per-element arithmetic)
+@pytest.mark.parametrize("L,ncmax", [(14, 600), (16, 1500)])
+def test_coarse_inverse_paths_agree(gpu_lib, monkeypatch, L, ncmax):
+    # the coarse inverse three ways: blocked Gauss-Jordan (default, panels of 32 columns,
+    # rank-32 updates), one launch per column with implicit pivoting (AJ_GJ_UNBLOCKED) and
+    # the swap-based two-launch reference (AJ_GJ_STEPS).  The last two run the same
+    # per-element arithmetic (bit for bit); the blocked one sums each panel's updates in a
+    # different order (agreement to rounding; ragged last panel when coarse_n % 32 != 0)
     import torch
-    L = 14
     eps_g = gpu_eps(gpu_lib, L, 16.5, 3)
     r = T(rand_vec(L ** 3, 8))
-    zs = []
-    for steps in (False, True):
-        if steps:
+    zs = {}
+    for mode in ("blocked", "unblocked", "steps"):
+        monkeypatch.delenv("AJ_GJ_UNBLOCKED", raising=False)
+        monkeypatch.delenv("AJ_GJ_STEPS", raising=False)
+        if mode == "unblocked":
+            monkeypatch.setenv("AJ_GJ_UNBLOCKED", "1")
+        if mode == "steps":
             monkeypatch.setenv("AJ_GJ_STEPS", "1")
-        K = gpu_lib.Precond(eps_g, L, -1.0, 0.0, gpu_lib.default_precond_params(n_coarse_max=600))
+        K = gpu_lib.Precond(eps_g, L, -1.0, 0.0, gpu_lib.default_precond_params(n_coarse_max=ncmax))
         assert K.info()["coarse_n"] > 100
         z = torch.empty_like(r)
         K.apply(z, r)
         K.free()
-        zs.append(z)
-    assert torch.equal(zs[0], zs[1])
+        zs[mode] = z
+    assert torch.equal(zs["unblocked"], zs["steps"])
+    assert torch.linalg.norm(zs["blocked"] - zs["steps"]) <= 1e-12 * torch.linalg.norm(zs["steps"])
+
+
+def test_coarse_inverse_blocked_vs_numpy(gpu_lib):
+    # the blocked dense inverse against numpy on the oracle's own coarse Schur complement:
+    # the GPU apply of a level-free preconditioner (n_coarse_max >= n: the whole matrix is
+    # the coarse block) is (A - sigma I)^{-1} r
+    import torch
+    L = 10
+    eps = an.disorder(L, 16.5, 5)
+    p = gpu_lib.default_precond_params(n_coarse_max=L ** 3, dense_cap=L ** 3)
+    K = gpu_lib.Precond(gpu_eps(gpu_lib, L, 16.5, 5), L, -1.0, 0.3, p)
+    assert K.info()["levels"] == 0 and K.info()["coarse_n"] == L ** 3
+    r = rand_vec(L ** 3, 9)
+    z = torch.empty(L ** 3, dtype=torch.float64, device="cuda")
+    K.apply(z, T(r))
+    K.free()
+    A = an.matrix(L, eps, hop=-1.0, sigma=0.3).toarray()
+    zr = np.linalg.solve(A, r)
+    assert np.linalg.norm(N(z) - zr) <= 1e-10 * np.linalg.norm(zr)
 
 
 def test_precond_exactness_limit_gpu(gpu_lib):

@@ -52,7 +52,7 @@ def test_precond_slab_parity(gpu_lib, L, world, W, seed):
     hop, sigma = -1.0, 0.0
     eps = an.disorder(L, W, seed)
     p = gpu_lib.default_precond_params(n_coarse_max=150)
-    td = p.tau_drop if p.tau_drop >= 0 else min(2e-3, 2e-3 * (50.0 / L) ** 2)
+    td = p.tau_drop if p.tau_drop >= 0 else 1.0 / (p.kappa * np.sqrt(float(L) ** 3))   # DESIGN.md R12
     ts = min(0.05, 40 * td)
     for r in range(world):
         z0, nz = slab.slab_bounds(L, r, world)

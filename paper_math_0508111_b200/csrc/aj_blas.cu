@@ -75,6 +75,10 @@ ProfScope::ProfScope(int c, double by, cudaStream_t s) : cat(c), bytes(by), st(s
     AJ_CUDA(cudaEventRecord(r->a, s));
   rec = r;
 }
+void ProfScope::set_bytes(double b) {
+  bytes = b;
+  if (rec) ((ProfRec*)rec)->bytes = b;
+}
 ProfScope::~ProfScope() {
   if (!rec) return;
   ProfRec* r = (ProfRec*)rec;

@@ -49,6 +49,7 @@ struct ProfScope {
   void* rec;
   ProfScope(int cat, double bytes, cudaStream_t st);
   ~ProfScope();
+  void set_bytes(double b);  // the byte model once it is known (the setup's work model)
 };
 enum { PROF_SPMV = 0, PROF_PREC = 1, PROF_SETUP = 2, PROF_SQMR = 3, PROF_JD = 4 };
 

@@ -2094,6 +2094,7 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
     I.level_pairs[l] = v.npairs;
     I.level_nnzS[l] = v.nnzS;
   }
+  ps.set_bytes(I.setup_bytes);  // live profile of the setup phase: its work model (DESIGN.md sect. 4)
   I.setup_ms = ms;
   I.tau_drop = P.tau_drop;
   I.tau_strong = P.tau_strong;

@@ -255,7 +255,7 @@ __host__ __device__ constexpr size_t schur_words() {
 }
 
 template <int G, int GROUPS, int T, int BM, bool GTAB, bool CAN_OVF>
-__global__ void __launch_bounds__(G * GROUPS)
+__global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register cap (tables limit the CTAs per SM)
     k_schur_rows(int nrows, const int32_t* __restrict__ rowlist, SchurArgs a, int32_t* __restrict__ scratch_all,
                  int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, int* __restrict__ err,
                  unsigned long long* __restrict__ products) {
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(G * GROUPS)
       double av[U], na_[U];
       int64_t e0 = 0, e1 = 0, ne0 = 0, ne1 = 0;
       double l = 0.0, nl_ = 0.0;
-      auto load_item = [&](int j, int64_t& f0, int64_t& f1, double& lv, int32_t* ccv, double* avv) {
+      auto load_item = [&](int j, int64_t& f0, int64_t& f1, double& lv, int32_t (&ccv)[U], double (&avv)[U]) {
         const int i = items[j];
         f0 = Xe0[i];
         f1 = Xe1[i];
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(G * GROUPS)
           avv[k] = (e < f1) ? a.FCval[e] : 0.0;
         }
       };
-      auto apply = [&](const int32_t* ccv, const double* avv, double lv) {
+      auto apply = [&](const int32_t (&ccv)[U], const double (&avv)[U], double lv) {
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           if (ccv[k] < 0) continue;

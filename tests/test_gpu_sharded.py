@@ -261,3 +261,28 @@ def test_nccl_comm_world1(gpu_lib):
         c.free()
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- bench.py --gpus 2 plumbing
+@pytest.mark.timeout(900)
+def test_bench_sharded_two_ranks_one_gpu():
+    # bench.py's N>1 path end to end (torchrun, 2 ranks, ONE lattice sharded into z-slabs):
+    # both ranks on cuda:0 with the torch.distributed comm (gloo, host-staged) -- plumbing
+    # only; the product runs the library's NCCL comm, one GPU per rank
+    import subprocess
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--comm", "torch", "--config", "0", "--steps", "2", "--warmup", "1",
+           "--large", "", "--big-L", "0", "--no-cpu-baseline"]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0"))
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=800, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert "sharded over 2 ranks" in d["config"]["parallelism"]
+    assert d["jd"]["max_resid_rel"] <= 1e-8
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "eigs_config0.json")))
+    assert np.allclose(np.sort(d["jd"]["eigenvalues"]), np.sort(gold["eigenvalues"]), rtol=0, atol=1e-9)

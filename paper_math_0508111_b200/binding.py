@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libanderson_jd.so")
+LIB_PATH = os.environ.get("AJ_LIB") or os.path.join(HERE, "libanderson_jd.so")  # AJ_LIB: experiments only
 
 AJ_OK, AJ_ERR_ARG, AJ_ERR_CUDA, AJ_ERR_BREAKDOWN, AJ_ERR_NOCONV, AJ_ERR_CAPACITY = range(6)
 

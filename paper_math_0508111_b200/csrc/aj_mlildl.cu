@@ -1005,7 +1005,10 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-constexpr int PREF = 8;  // factor entries per lane prefetched before the dependency wait
+#ifndef AJ_PREF
+#define AJ_PREF 8
+#endif
+constexpr int PREF = AJ_PREF;  // factor entries per lane prefetched before the dependency wait
 
 // sum_q val[e_q] * src[col[e_q]] over e_q = b + q*G < e1, q < PREF: all index/value loads
 // issued before the gathers (memory-level parallelism instead of a dependent chain per entry);

@@ -52,6 +52,22 @@
 
 namespace aj {
 
+// -DAJ_SCHUR_PROF (experiments only): per-phase clock64 sums of k_schur_rows, lane 0 of every
+// group, accumulated in g_schur_prof[phase] and printed by schur_prof_dump()
+#ifdef AJ_SCHUR_PROF
+__device__ unsigned long long g_schur_prof[16];
+#define SPROF_DECL long long sp_t0 = clock64(), sp_t1
+#define SPROF(ph)                                                          \
+  do {                                                                     \
+    sp_t1 = clock64();                                                     \
+    if (tid == 0) atomicAdd(&g_schur_prof[ph], (unsigned long long)(sp_t1 - sp_t0)); \
+    sp_t0 = sp_t1;                                                         \
+  } while (0)
+#else
+#define SPROF_DECL
+#define SPROF(ph)
+#endif
+
 namespace {
 constexpr int TBs = 256;
 
@@ -297,6 +313,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     const int cp = rowlist[ri];
     const int c = a.cidx[cp];
     const int64_t lo = a.ptr[c], hi = a.ptr[c + 1];
+    SPROF_DECL;
     if (tid == 0) {
       s_cnt[grp] = 0;
       s_nvt[grp] = 0;
@@ -347,6 +364,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       }
     }
     gsync<G, GROUPS>();
+    SPROF(0);
     // ---- (A2) virtual terms in ascending block key, accumulated into l^v (serial)
     const int nvt = s_nvt[grp];
     if (nvt > 0) {
@@ -376,6 +394,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       }
       gsync<G, GROUPS>();
     }
+    SPROF(1);
     // ---- (A3) empty the table; the L row sorted by x, with the FC range of each x
     const int nl = s_cnt[grp];
     for (int pos = tid; pos < nl; pos += G) {
@@ -392,6 +411,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       gsync<G, GROUPS>();
       if (nl > 1) group_bitonic<G, GROUPS>(sk, sp, P, tid);
     }
+    SPROF(2);
     for (int i = tid; i < nl; i += G) {
       const int pos = sp[i];
       const int32_t x = Lx[pos];
@@ -418,6 +438,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     }
     if (tid == 0) s_cnt[grp] = 0;
     gsync<G, GROUPS>();
+    SPROF(3);
     // ---- (B) s_cc' = a^_cc' (upper triangle c' >= c: the lower one is its mirror)
     for (int64_t e = lo + tid; e < hi; e += G) {
       const int32_t cu = a.cmap[a.col[e]];
@@ -429,6 +450,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
         vals[sl] = a.ah[e];
     }
     gsync<G, GROUPS>();
+    SPROF(4);
     // ---- (C) real terms, x ascending; (D) virtual terms on the pattern, x ascending
     // work lists of (C) and (D): the sorted L-row positions with real / virtual terms
     if (tid == 0) {
@@ -515,6 +537,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
         }
       }
     }
+    SPROF(5);
     // ---- (E) collect through the slot list, empty the table, drop
     const bool full = CAN_OVF && (s_full[grp] != 0 || s_cnt[grp] > (T * 3) / 4);
     const int nc = min(s_cnt[grp], T);
@@ -546,7 +569,9 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       vals[t] = (t < kept) ? evals[t] : 0.0;
     }
     gsync<G, GROUPS>();
+    SPROF(6);
     group_bitonic<G, GROUPS>(tab, vals, P, tid);
+    SPROF(7);
     if (tid == 0) {
       atomicAdd(products, nprod);
       const unsigned long long base = atomicAdd(a.cursor, (unsigned long long)kept);
@@ -565,6 +590,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     }
     gsync<G, GROUPS>();
     for (int t = tid; t < P; t += G) tab[t] = -1;
+    SPROF(8);
     // ---- the L row (x ascending), L_cx = l^r + l^v, |L| < tau dropped (first warp)
     if (tid < 32) {
       const int lane = tid;
@@ -602,6 +628,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       }
     }
     gsync<G, GROUPS>();
+    SPROF(9);
   }
 }
 
@@ -635,6 +662,31 @@ using TierC8 = Tier<128, 1, 8192, 4096, false, false>;   // 96 KB: 2 rows per SM
 using TierC16 = Tier<256, 1, 16384, 4096, false, true>;  // 192 KB: 1 row per SM, may overflow
 using TierG = Tier<256, 1, 65536, 8192, true, true>;     // global-memory table
 
+// Fork / join for the tier kernels: rows of different tiers are independent (disjoint output
+// runs through the global cursors), so the tiers run concurrently on side streams -- on the deep
+// levels each tier alone fills only a few SMs.  Streams and events are cached per host thread
+// and device (a stream belongs to the device that was current when it was created).
+struct TierStreams {
+  cudaStream_t s[NTIER] = {};
+  cudaEvent_t fork = nullptr, done[NTIER] = {};
+};
+static TierStreams& tier_streams() {
+  constexpr int kMaxDev = 64;
+  thread_local TierStreams ts[kMaxDev];
+  int dev = 0;
+  AJ_CUDA(cudaGetDevice(&dev));
+  AJ_REQUIRE(dev >= 0 && dev < kMaxDev, AJ_ERR_CUDA, "device ordinal out of range");
+  TierStreams& t = ts[dev];
+  if (!t.fork) {
+    AJ_CUDA(cudaEventCreateWithFlags(&t.fork, cudaEventDisableTiming));
+    for (int k = 0; k < NTIER; ++k) {
+      AJ_CUDA(cudaStreamCreateWithFlags(&t.s[k], cudaStreamNonBlocking));
+      AJ_CUDA(cudaEventCreateWithFlags(&t.done[k], cudaEventDisableTiming));
+    }
+  }
+  return t;
+}
+
 template <typename T>
 static T read1(const T* d, cudaStream_t st) {
   T h;
@@ -643,6 +695,23 @@ static T read1(const T* d, cudaStream_t st) {
   return h;
 }
 }  // namespace
+
+#ifdef AJ_SCHUR_PROF
+static void schur_prof_dump(const char* tag, cudaStream_t st) {
+  unsigned long long h[16];
+  cudaStreamSynchronize(st);
+  cudaMemcpyFromSymbol(h, g_schur_prof, sizeof(h));
+  static const char* nm[10] = {"A1 L row", "A2 virtual", "A3 sort L", "A3 FC ranges", "B row insert", "C/D products",
+                               "E collect", "E sort", "E write S", "L row write"};
+  double tot = 0;
+  for (int i = 0; i < 10; ++i) tot += (double)h[i];
+  fprintf(stderr, "[schur prof] %s:", tag);
+  for (int i = 0; i < 10; ++i) fprintf(stderr, " %s %.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
+  fprintf(stderr, "\n");
+  memset(h, 0, sizeof(h));
+  cudaMemcpyToSymbol(g_schur_prof, h, sizeof(h));
+}
+#endif
 
 void schur_level(const SchurIn& in, SchurOut& out, cudaStream_t st) {
   const int nC = in.nC, nF = in.nF;
@@ -730,7 +799,7 @@ void schur_level(const SchurIn& in, SchurOut& out, cudaStream_t st) {
   a.cursor = cursor;
   a.lcursor = cursor + 1;
 
-  // per tier: resident grid and scratch words (one scratch buffer, tiers run in sequence)
+  // per tier: resident grid and scratch words (one region of the scratch buffer per tier)
   struct TierRun {
     int groups;
     size_t words;
@@ -747,13 +816,26 @@ void schur_level(const SchurIn& in, SchurOut& out, cudaStream_t st) {
   tr[TIER_C8] = {1, TierC8::words(), TierC8::resident_ctas()};
   tr[TIER_C16] = {1, TierC16::words(), TierC16::resident_ctas()};
   tr[TIER_G] = {1, TierG::words(), num_sms()};
-  size_t scr_words = 2;
+  size_t scr_words = 2, scr_off[NTIER] = {};
   int grid[NTIER];
+  int nactive = 0;
   for (int t = 0; t < NTIER; ++t) {
     grid[t] = std::max(1, std::min(tr[t].ctas, ceil_div(std::max(cnt[t], 1), tr[t].groups)));
-    if (cnt[t] > 0 && t != TIER_G) scr_words = std::max(scr_words, (size_t)grid[t] * tr[t].groups * tr[t].words);
+    scr_off[t] = scr_words;
+    if (cnt[t] > 0 && t != TIER_G) {
+      scr_words += (size_t)grid[t] * tr[t].groups * tr[t].words;
+      ++nactive;
+    }
   }
   int32_t* scratch = dalloc<int32_t>(scr_words, st);
+  // concurrent tiers when more than one has rows and none fills the GPU by itself for long
+  // (AJ_SCHUR_SERIAL=1, testing: one stream)
+#ifdef AJ_SCHUR_PROF
+  const bool fork = false;
+#else
+  const bool fork = nactive > 1 && !getenv("AJ_SCHUR_SERIAL");
+#endif
+  TierStreams* tsp = fork ? &tier_streams() : nullptr;
   int32_t* scratchG = nullptr;
   int* err = ctr + NTIER + 1;
 
@@ -773,15 +855,42 @@ void schur_level(const SchurIn& in, SchurOut& out, cudaStream_t st) {
     AJ_CUDA(cudaMemsetAsync(cursor, 0, 3 * sizeof(unsigned long long), st));
     AJ_CUDA(cudaMemsetAsync(ctr + NTIER, 0, 2 * sizeof(int), st));
     auto L0 = [&](int t) { return lists + (size_t)t * nC1; };
-    if (cnt[TIER_W1]) TierW1::launch(cnt[TIER_W1], L0(TIER_W1), a, scratch, grid[TIER_W1], nullptr, nullptr, err, cursor + 2, st);
-    if (cnt[TIER_W2]) TierW2::launch(cnt[TIER_W2], L0(TIER_W2), a, scratch, grid[TIER_W2], nullptr, nullptr, err, cursor + 2, st);
-    if (cnt[TIER_P4]) TierP4::launch(cnt[TIER_P4], L0(TIER_P4), a, scratch, grid[TIER_P4], nullptr, nullptr, err, cursor + 2, st);
-    if (cnt[TIER_C8]) TierC8::launch(cnt[TIER_C8], L0(TIER_C8), a, scratch, grid[TIER_C8], nullptr, nullptr, err, cursor + 2, st);
+#ifdef AJ_SCHUR_PROF
+#define SDUMP(name, rows)                                                              \
+  if ((rows) > 0 && nC >= 200000) {                                                    \
+    char tg[64];                                                                       \
+    snprintf(tg, sizeof tg, "nC=%d tier %s rows=%d", nC, name, (int)(rows));           \
+    schur_prof_dump(tg, st);                                                           \
+  }
+#else
+#define SDUMP(name, rows)
+#endif
+    if (fork) AJ_CUDA(cudaEventRecord(tsp->fork, st));
+    auto TS = [&](int t) -> cudaStream_t {  // the tier's stream, ordered after the work queued on st so far
+      if (!fork) return st;
+      AJ_CUDA(cudaStreamWaitEvent(tsp->s[t], tsp->fork, 0));
+      return tsp->s[t];
+    };
+    auto SCR = [&](int t) { return scratch + scr_off[t]; };
+    // the largest tables first: their few long rows are the tail of the level
+    if (cnt[TIER_C16]) TierC16::launch(cnt[TIER_C16], L0(TIER_C16), a, SCR(TIER_C16), grid[TIER_C16], ovf, ctr + NTIER, err, cursor + 2, TS(TIER_C16));
+    SDUMP("C16", cnt[TIER_C16]);
+    if (cnt[TIER_C8]) TierC8::launch(cnt[TIER_C8], L0(TIER_C8), a, SCR(TIER_C8), grid[TIER_C8], nullptr, nullptr, err, cursor + 2, TS(TIER_C8));
+    SDUMP("C8", cnt[TIER_C8]);
+    if (cnt[TIER_P4]) TierP4::launch(cnt[TIER_P4], L0(TIER_P4), a, SCR(TIER_P4), grid[TIER_P4], nullptr, nullptr, err, cursor + 2, TS(TIER_P4));
+    SDUMP("P4", cnt[TIER_P4]);
+    if (cnt[TIER_W2]) TierW2::launch(cnt[TIER_W2], L0(TIER_W2), a, SCR(TIER_W2), grid[TIER_W2], nullptr, nullptr, err, cursor + 2, TS(TIER_W2));
+    SDUMP("W2", cnt[TIER_W2]);
+    if (cnt[TIER_W1]) TierW1::launch(cnt[TIER_W1], L0(TIER_W1), a, SCR(TIER_W1), grid[TIER_W1], nullptr, nullptr, err, cursor + 2, TS(TIER_W1));
+    SDUMP("W1", cnt[TIER_W1]);
+    if (fork)
+      for (int t = TIER_W1; t <= TIER_C16; ++t)
+        if (cnt[t]) {
+          AJ_CUDA(cudaEventRecord(tsp->done[t], tsp->s[t]));
+          AJ_CUDA(cudaStreamWaitEvent(st, tsp->done[t], 0));
+        }
     int nov = 0;
-    if (cnt[TIER_C16]) {
-      TierC16::launch(cnt[TIER_C16], L0(TIER_C16), a, scratch, grid[TIER_C16], ovf, ctr + NTIER, err, cursor + 2, st);
-      nov = read1(ctr + NTIER, st);
-    }
+    if (cnt[TIER_C16]) nov = read1(ctr + NTIER, st);
     // tier G: the rows routed there plus the C16 overflows
     int ng = cnt[TIER_G];
     if (nov > 0) {

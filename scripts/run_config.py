@@ -37,6 +37,8 @@ def main():
                      ("kappa", "AJ_KAPPA")):
         if env in os.environ:
             setattr(pp, key, float(os.environ[env]))
+    if "AJ_F32" in os.environ:
+        pp.factor_fp32 = int(os.environ["AJ_F32"])
     if "AJ_DENSE_CAP" in os.environ:
         pp.dense_cap = int(os.environ["AJ_DENSE_CAP"])
     if "AJ_NCOARSE" in os.environ:

@@ -1003,12 +1003,26 @@ __global__ void k_gj_extract(int n, const double* __restrict__ M, double* __rest
 // does not depend on its predecessor -- row bounds, indices, factor values -- before
 // griddepcontrol.wait; only the gathers of the predecessor's output come after it.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#ifdef AJ_NO_PDL_WAIT  // timing diagnostic only (results are garbage): the levels overlap freely
+__device__ __forceinline__ void pdl_wait() {}
+#else
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
 
 #ifndef AJ_PREF
 #define AJ_PREF 8
 #endif
 constexpr int PREF = AJ_PREF;  // factor entries per lane prefetched before the dependency wait
+
+// factor entries are read once per apply: streaming (evict-first) loads, so the stream does not
+// push the gather vectors (rF, zn: re-read by many rows) out of L1 / L2
+#ifdef AJ_NO_STREAM_LD
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return *p; }
+#else
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+#endif
 
 // sum_q val[e_q] * src[col[e_q]] over e_q = b + q*G < e1, q < PREF: all index/value loads
 // issued before the gathers (memory-level parallelism instead of a dependent chain per entry);
@@ -1021,8 +1035,8 @@ __device__ __forceinline__ double gather_batch(int64_t b, int64_t e1, const int3
 #pragma unroll
   for (int q = 0; q < PREF; ++q) {
     const int64_t e = b + (int64_t)q * G;
-    c[q] = (e < e1) ? col[e] : -1;
-    v[q] = (e < e1) ? (double)val[e] : 0.0;
+    c[q] = (e < e1) ? ld_stream(&col[e]) : -1;
+    v[q] = (e < e1) ? (double)ld_stream(&val[e]) : 0.0;
   }
   double acc = 0.0;
 #pragma unroll
@@ -1057,8 +1071,8 @@ __global__ void __launch_bounds__(TB)
 #pragma unroll
     for (int q = 0; q < PREF; ++q) {
       const int64_t e = e0 + (int64_t)q * G;
-      pc[q] = (e < e1) ? Lcol[e] : -1;
-      pv[q] = (e < e1) ? (double)Lval[e] : 0.0;
+      pc[q] = (e < e1) ? ld_stream(&Lcol[e]) : -1;
+      pv[q] = (e < e1) ? (double)ld_stream(&Lval[e]) : 0.0;
     }
   }
   pdl_wait();
@@ -1117,8 +1131,8 @@ __global__ void __launch_bounds__(TB)
 #pragma unroll
     for (int q = 0; q < PREF; ++q) {
       const int64_t e = e0 + (int64_t)q * G;
-      pc[q] = (e < e1) ? LTcol[e] : -1;
-      pv[q] = (e < e1) ? (double)LTval[e] : 0.0;
+      pc[q] = (e < e1) ? ld_stream(&LTcol[e]) : -1;
+      pv[q] = (e < e1) ? (double)ld_stream(&LTval[e]) : 0.0;
     }
     if (lane == 0) {
       i = fidx[fp];
@@ -1385,6 +1399,366 @@ __global__ void __launch_bounds__(TB, 6)
   }
 }
 
+// ---- persistent ring apply (DESIGN.md sect. 4) ------------------------------------------
+// Large levels: one CTA per SM owns a run of consecutive rows holding ~1/grid of the level's
+// factor entries (row partition `part`, balanced by entries at setup).  A producer warp streams
+// the CTA's contiguous (index, value) range through a ring of RNST shared-memory stages with 1-D
+// bulk copies (full/empty mbarrier pair per stage); RNW consumer warps walk the rows in tiles of
+// RNW * 32 / G rows, each warp at its own pace: it waits for the stages holding its rows'
+// entries, gathers the predecessor's output (PREF independent gathers per batch), reduces over
+// the G lanes of a row and writes.  Every warp passes every stage in order (wait full, then
+// arrive empty), so a stage is refilled only when all warps are past it.  The factor stream
+// never waits behind a row pointer or a gather; the first RNST stages are issued before
+// griddepcontrol.wait, and a CTA takes less than half an SM's shared memory and threads so the
+// next level's CTAs are resident (prefetching) while this level runs.  Row metadata is loaded
+// one tile ahead.
+#ifndef AJ_RCAP
+#define AJ_RCAP 2048
+#define AJ_RNST 4
+#define AJ_RNW 16
+#define AJ_RING_CTAS 1
+#endif
+#ifndef AJ_RING_MINB
+#define AJ_RING_MINB 2  // two resident CTAs per SM: this level's and the next level's (prefetching)
+#endif
+constexpr int RCAP = AJ_RCAP;  // entries per stage: 8 KB indices + 16 KB fp64 values
+constexpr int RNST = AJ_RNST;  // stages (96 KB)
+constexpr int RNW = AJ_RNW;    // consumer warps
+constexpr int RING_CTAS = AJ_RING_CTAS;  // ring CTAs per SM
+constexpr int RTB = RNW * 32 + 32;  // + the producer warp
+
+template <typename TV>
+struct RingBuf {
+  int32_t col[RCAP];
+  TV val[RCAP];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct RingPlan {
+  int64_t SB, SE;  // 4-entry-aligned hull of the CTA's entry range that the ring covers
+  int nch;
+};
+__device__ __forceinline__ RingPlan ring_plan(int64_t E0, int64_t E1, int64_t nnz) {
+  RingPlan p;
+  p.SB = E0 & ~int64_t(3);
+  p.SE = min((E1 + 3) & ~int64_t(3), nnz & ~int64_t(3));  // never past the last full 16-byte granule
+  p.nch = p.SE > p.SB ? (int)((p.SE - p.SB + RCAP - 1) / RCAP) : 0;
+  return p;
+}
+
+// producer (one lane): all chunks of the CTA's range in order, a stage refilled once every
+// consumer warp has arrived on its empty barrier
+template <typename TV>
+__device__ __forceinline__ void ring_produce(const RingPlan& p, RingBuf<TV>* sb, uint64_t* full, uint64_t* empty,
+                                             const int32_t* col, const TV* val) {
+  for (int ch = 0; ch < p.nch; ++ch) {
+    const int s = ch % RNST;
+    if (ch >= RNST) {
+      mbar_wait(&empty[s], (uint32_t)(((ch / RNST) - 1) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const int64_t cs = p.SB + (int64_t)ch * RCAP, ce = min(p.SE, cs + RCAP);
+    const uint32_t n = (uint32_t)(ce - cs);
+    mbar_expect_tx(&full[s], n * (uint32_t)(4 + sizeof(TV)));
+    bulk_g2s(sb[s].col, col + cs, n * 4u, &full[s]);
+    bulk_g2s(sb[s].val, val + cs, n * (uint32_t)sizeof(TV), &full[s]);
+  }
+}
+
+// consumer-side state of one warp: `cur` = first chunk it has not released yet
+struct RingWarp {
+  int cur = 0;
+};
+template <typename TV>
+__device__ __forceinline__ void ring_skip_to(RingWarp& w, int ch, uint64_t* full, uint64_t* empty) {
+  for (; w.cur < ch; ++w.cur) {
+    mbar_wait(&full[w.cur % RNST], (uint32_t)((w.cur / RNST) & 1));
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[w.cur % RNST]);
+  }
+}
+
+// this lane's partial sum over its row's entries e = e0 + lane + m G in [e0, e1), read from the
+// ring; [w0, w1) is the warp's entry range of the tile (warp-uniform).  Entries >= SE (past the
+// last full granule of the array) come from global memory.
+template <int G, typename TV>
+__device__ __forceinline__ double ring_row_sum(RingWarp& w, const RingPlan& p, RingBuf<TV>* sb, uint64_t* full,
+                                               uint64_t* empty, int64_t w0, int64_t w1, bool act, int64_t e0,
+                                               int64_t e1, int lane, const int32_t* __restrict__ col,
+                                               const TV* __restrict__ val, const double* __restrict__ src) {
+  double acc = 0.0;
+  const int64_t wh = min(w1, p.SE);
+  if (wh > w0) {
+    const int chA = (int)((w0 - p.SB) / RCAP), chB = (int)((wh - 1 - p.SB) / RCAP);
+    ring_skip_to<TV>(w, chA, full, empty);
+    for (int ch = chA; ch <= chB; ++ch) {
+      const int s = ch % RNST;
+      const int64_t cs = p.SB + (int64_t)ch * RCAP, ce = min(p.SE, cs + RCAP);
+      mbar_wait(&full[s], (uint32_t)((ch / RNST) & 1));
+      if (act) {
+        const int64_t lo = max(e0, cs), hi = min(e1, ce);
+        int64_t e = e0 + lane;
+        if (e < lo) e += ((lo - e + G - 1) / G) * G;
+        const RingBuf<TV>* b = sb + s;
+        for (; e < hi; e += (int64_t)PREF * G) {
+          int32_t c[PREF];
+          double v[PREF];
+#pragma unroll
+          for (int q = 0; q < PREF; ++q) {
+            const int64_t ee = e + (int64_t)q * G;
+            c[q] = (ee < hi) ? b->col[ee - cs] : -1;
+            v[q] = (ee < hi) ? (double)b->val[ee - cs] : 0.0;
+          }
+          double part = 0.0;
+#pragma unroll
+          for (int q = 0; q < PREF; ++q)
+            if (c[q] >= 0) part += v[q] * __ldg(&src[c[q]]);
+          acc += part;
+        }
+      }
+      if (ch < chB) {  // done with this stage; the last one stays held for the next tile
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        w.cur = ch + 1;
+      }
+    }
+  }
+  if (act && e1 > p.SE) {
+    int64_t e = e0 + lane;
+    if (e < p.SE) e += ((p.SE - e + G - 1) / G) * G;
+    for (; e < e1; e += G) acc += (double)val[e] * __ldg(&src[col[e]]);
+  }
+  return acc;
+}
+
+// The backward ring kernel's per-row right-hand side, computed by extra CTAs of the level's
+// FORWARD kernel (it needs only the level's input r): yv_f = B~^{-1}-row of D r on the pivot block
+// (1x1 / 2x2 part plus the virtual couplings, reading R17), dF_f = D_f.  The backward epilogue is
+// then z_f = dF_f (yv_f - sum), with every operand indexed by the pivot row (coalesced, loaded a
+// tile ahead) instead of three dependent gathers per row.
+struct PrepArgs {
+  int nF, nparts;
+  const int32_t* fidx;
+  const int32_t* partner;
+  const double *b11, *b12;
+  const int64_t* Vptr;
+  const int32_t* Vcol;
+  const double* Vval;
+  const double* rF;
+  double *yv, *dF;
+};
+__device__ __forceinline__ void bwd_prep_rows(const PrepArgs& a, const double* __restrict__ D,
+                                              const double* __restrict__ r, int first, int stride) {
+  for (int fp = first; fp < a.nF; fp += stride) {
+    const int i = a.fidx[fp];
+    const double Di = D[i];
+    double y = a.b11[i] * (Di * (a.rF ? a.rF[fp] : r[i]));
+    const int p = a.partner[i];
+    if (p >= 0) y += a.b12[i] * (D[p] * r[p]);
+    if (a.Vptr)
+      for (int64_t e = a.Vptr[i]; e < a.Vptr[i + 1]; ++e) {
+        const int32_t v = a.Vcol[e];
+        y += a.Vval[e] * (D[v] * r[v]);
+      }
+    a.yv[fp] = y;
+    a.dF[fp] = Di;
+  }
+}
+
+template <int G, typename TV>
+__global__ void __launch_bounds__(RTB, AJ_RING_MINB)
+    k_apply_fwd_r(int64_t nnz, const int32_t* __restrict__ part, const int32_t* __restrict__ cidx,
+                  const double* __restrict__ D, const double* __restrict__ r, const double* __restrict__ gsrc,
+                  const int64_t* __restrict__ Lptr, const int32_t* __restrict__ Lcol, const TV* __restrict__ Lval,
+                  double* __restrict__ rn, double* __restrict__ rFn, const int32_t* __restrict__ fmapn,
+                  PrepArgs prep) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  RingBuf<TV>* sb = reinterpret_cast<RingBuf<TV>*>(smraw);
+  __shared__ __align__(8) uint64_t full[RNST], empty[RNST];
+  pdl_launch_dependents();
+  if ((int)blockIdx.x >= prep.nparts) {  // prep CTAs
+    pdl_wait();
+    bwd_prep_rows(prep, D, r, ((int)blockIdx.x - prep.nparts) * RTB + (int)threadIdx.x,
+                  ((int)gridDim.x - prep.nparts) * RTB);
+    return;
+  }
+  const int row0 = part[blockIdx.x], row1 = part[blockIdx.x + 1];
+  const RingPlan pl = ring_plan(Lptr[row0], Lptr[row1], nnz);
+  const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], RNW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == RNW) {
+    if (l32 == 0) ring_produce<TV>(pl, sb, full, empty, Lcol, Lval);
+    return;
+  }
+  constexpr int RW = 32 / G, RT = RNW * RW;
+  const int sub = l32 / G, lane = l32 % G;
+  int wr = row0 + warp * RW;  // the warp's first row of the tile
+  int cp = wr + sub;
+  bool act = cp < row1;
+  int64_t e0 = 0, e1 = 0;
+  int c = 0, fn = -1;
+  if (act) {
+    e0 = Lptr[cp];
+    e1 = Lptr[cp + 1];
+    c = cidx[cp];
+    if (rFn && lane == 0) fn = fmapn[cp];
+  }
+  pdl_wait();
+  RingWarp w;
+  for (; wr < row1; wr += RT) {
+    // the next tile's row bounds and indices, one tile ahead
+    const int cpn = cp + RT;
+    const bool actn = cpn < row1;
+    int64_t e0n = 0, e1n = 0;
+    int cn = 0, fnn = -1;
+    if (actn) {
+      e0n = Lptr[cpn];
+      e1n = Lptr[cpn + 1];
+      cn = cidx[cpn];
+      if (rFn && lane == 0) fnn = fmapn[cpn];
+    }
+    double Dc = 0.0, rc = 0.0;
+    if (act && lane == 0) {
+      Dc = D[c];
+      rc = r[c];
+    }
+    const int last = (min(RW, row1 - wr) - 1) * G;  // a lane of the warp's last active row
+    const int64_t w0 = __shfl_sync(0xffffffffu, e0, 0), w1 = __shfl_sync(0xffffffffu, e1, last);
+    double acc = ring_row_sum<G, TV>(w, pl, sb, full, empty, w0, w1, act, e0, e1, lane, Lcol, Lval, gsrc);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (act && lane == 0) {
+      const double v = Dc * rc - acc;
+      rn[cp] = v;
+      if (fn >= 0) rFn[fn] = v;
+    }
+    cp = cpn;
+    act = actn;
+    e0 = e0n;
+    e1 = e1n;
+    c = cn;
+    fn = fnn;
+  }
+  ring_skip_to<TV>(w, pl.nch, full, empty);  // pass the remaining stages so the producer can finish
+}
+
+// backward: CTAs [0, nparts) take the pivot rows through the ring (source zn, the next level's
+// solution), CTAs >= nparts copy the coarse solution back (z_c = D_c zn_c', RCPY nodes each)
+constexpr int RCPY = 4;
+template <int G, typename TV>
+__global__ void __launch_bounds__(RTB, AJ_RING_MINB)
+    k_apply_bwd_r(int nC, int nparts, int64_t nnz, const int32_t* __restrict__ part,
+                  const int32_t* __restrict__ fidx, const int32_t* __restrict__ cidx, const double* __restrict__ D,
+                  const double* __restrict__ yv, const double* __restrict__ dF, const int64_t* __restrict__ LTptr,
+                  const int32_t* __restrict__ LTcol, const TV* __restrict__ LTval, const double* __restrict__ zn,
+                  double* __restrict__ z) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  RingBuf<TV>* sb = reinterpret_cast<RingBuf<TV>*>(smraw);
+  __shared__ __align__(8) uint64_t full[RNST], empty[RNST];
+  pdl_launch_dependents();
+  if ((int)blockIdx.x >= nparts) {  // coarse part
+    const int base = ((int)blockIdx.x - nparts) * (RTB * RCPY) + (int)threadIdx.x;
+    int i[RCPY];
+    double Di[RCPY];
+#pragma unroll
+    for (int q = 0; q < RCPY; ++q) {
+      const int cp = base + q * RTB;
+      i[q] = cp < nC ? cidx[cp] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < RCPY; ++q) Di[q] = i[q] >= 0 ? D[i[q]] : 0.0;
+    pdl_wait();
+#pragma unroll
+    for (int q = 0; q < RCPY; ++q)
+      if (i[q] >= 0) z[i[q]] = Di[q] * zn[base + q * RTB];
+    return;
+  }
+  const int row0 = part[blockIdx.x], row1 = part[blockIdx.x + 1];
+  const RingPlan pl = ring_plan(LTptr[row0], LTptr[row1], nnz);
+  const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], RNW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == RNW) {
+    if (l32 == 0) ring_produce<TV>(pl, sb, full, empty, LTcol, LTval);
+    return;
+  }
+  constexpr int RW = 32 / G, RT = RNW * RW;
+  const int sub = l32 / G, lane = l32 % G;
+  int wr = row0 + warp * RW;
+  int fp = wr + sub;
+  bool act = fp < row1;
+  int64_t e0 = 0, e1 = 0;
+  int i = 0;
+  if (act) {
+    e0 = LTptr[fp];
+    e1 = LTptr[fp + 1];
+    if (lane == 0) i = fidx[fp];
+  }
+  pdl_wait();
+  RingWarp w;
+  for (; wr < row1; wr += RT) {
+    const int fpn = fp + RT;
+    const bool actn = fpn < row1;
+    int64_t e0n = 0, e1n = 0;
+    int in = 0;
+    if (actn) {
+      e0n = LTptr[fpn];
+      e1n = LTptr[fpn + 1];
+      if (lane == 0) in = fidx[fpn];
+    }
+    double y = 0.0, Df = 0.0;
+    if (act && lane == 0) {
+      y = yv[fp];
+      Df = dF[fp];
+    }
+    const int last = (min(RW, row1 - wr) - 1) * G;
+    const int64_t w0 = __shfl_sync(0xffffffffu, e0, 0), w1 = __shfl_sync(0xffffffffu, e1, last);
+    double acc = ring_row_sum<G, TV>(w, pl, sb, full, empty, w0, w1, act, e0, e1, lane, LTcol, LTval, zn);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (act && lane == 0) z[i] = Df * (y - acc);
+    fp = fpn;
+    act = actn;
+    e0 = e0n;
+    e1 = e1n;
+    i = in;
+  }
+  ring_skip_to<TV>(w, pl.nch, full, empty);
+}
+
+// row partition of a CSR-like pointer array into nparts runs of ~equal entry counts
+__global__ void k_row_partition(int nrows, const int64_t* __restrict__ ptr, int nparts, int32_t* __restrict__ part) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nparts) return;
+  if (b == nparts) {
+    part[b] = nrows;
+    return;
+  }
+  const int64_t nnz = ptr[nrows], target = (nnz / nparts) * b + min((int64_t)b, nnz % nparts);
+  int lo = 0, hi = nrows;  // first row with ptr[row] >= target
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ptr[mid] >= target) hi = mid; else lo = mid + 1;
+  }
+  part[b] = lo;
+}
+
 // G lanes per row such that each lane holds ~per_lane entries: 8 on large levels
 // (streaming, more loads in flight per thread), 4 on small L2-resident ones (more
 // threads); measured at L = 50..200 (DESIGN.md sect. 4)
@@ -1396,6 +1770,22 @@ static int pick_group(double avg_len, int64_t nnz, int gmax = 32) {
   return g;
 }
 
+template <typename K, typename... Args>
+static void launch_pdl_block(K kernel, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  if (smem > 48 * 1024) AJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AJ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+  AJ_LAUNCHED();
+}
 template <typename K, typename... Args>
 static void launch_pdl_smem(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -1429,6 +1819,19 @@ static int pick_stages(int64_t nnz, int64_t rows, int g) {
 template <int G>
 static void fwd_g(const Level& v, const double* r, const double* gsrc, double* rn, double* rFn,
                   const int32_t* fmapn, int grid, cudaStream_t st) {
+  if (v.fpart) {  // persistent ring kernel, one CTA per partition run (+ the backward prep CTAs)
+    PrepArgs pa{v.nF, v.nfpart, v.fidx, v.partner, v.b11, v.b12, v.Vptr, v.Vcol, v.Vval, v.rF, v.yv, v.dF};
+    const int gridr = v.nfpart + (v.bpart ? std::max(1, std::min(num_sms(), ceil_div(v.nF, RTB))) : 0);
+    if (v.f32)
+      launch_pdl_block(k_apply_fwd_r<G, float>, gridr, RTB, RNST * sizeof(RingBuf<float>), st, v.nnzL,
+                       (const int32_t*)v.fpart, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc,
+                       (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const float*)v.Lval, rn, rFn, fmapn, pa);
+    else
+      launch_pdl_block(k_apply_fwd_r<G, double>, gridr, RTB, RNST * sizeof(RingBuf<double>), st, v.nnzL,
+                       (const int32_t*)v.fpart, (const int32_t*)v.cidx, (const double*)v.D, r, gsrc,
+                       (const int64_t*)v.Lptr, (const int32_t*)v.Lcol, (const double*)v.Lval, rn, rFn, fmapn, pa);
+    return;
+  }
   if (v.nst_f > 0) {
     if (v.f32)
       launch_pdl_smem(k_apply_fwd_s<G, float>, grid, v.nst_f * sizeof(StageBuf<float>), st, v.nC, v.nst_f, v.nnzL,
@@ -1449,6 +1852,22 @@ static void fwd_g(const Level& v, const double* r, const double* gsrc, double* r
 }
 template <int G>
 static void bwd_g(const Level& v, const double* r, const double* zn, double* z, int bF, int grid, cudaStream_t st) {
+  if constexpr (G <= 32) {
+    if (v.bpart) {  // persistent ring kernel (yv, dF from the level's forward kernel)
+      const int gridr = v.nbpart + ceil_div(v.nC, RTB * RCPY);
+      if (v.f32)
+        launch_pdl_block(k_apply_bwd_r<G, float>, gridr, RTB, RNST * sizeof(RingBuf<float>), st, v.nC, v.nbpart,
+                         v.nnzLT, (const int32_t*)v.bpart, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
+                         (const double*)v.D, (const double*)v.yv, (const double*)v.dF, (const int64_t*)v.LTptr,
+                         (const int32_t*)v.LTcol, (const float*)v.LTval, zn, z);
+      else
+        launch_pdl_block(k_apply_bwd_r<G, double>, gridr, RTB, RNST * sizeof(RingBuf<double>), st, v.nC, v.nbpart,
+                         v.nnzLT, (const int32_t*)v.bpart, (const int32_t*)v.fidx, (const int32_t*)v.cidx,
+                         (const double*)v.D, (const double*)v.yv, (const double*)v.dF, (const int64_t*)v.LTptr,
+                         (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z);
+      return;
+    }
+  }
   if (v.nst_b > 0) {
     if (v.f32)
       launch_pdl_smem(k_apply_bwd_s<G, float>, grid, v.nst_b * sizeof(StageBuf<float>), st, v.nF, v.nC, bF, v.nst_b,
@@ -1474,6 +1893,40 @@ static void bwd_g(const Level& v, const double* r, const double* zn, double* z, 
                (const double*)v.D, r, (const int32_t*)v.partner, (const double*)v.b11, (const double*)v.b12,
                (const int64_t*)v.LTptr, (const int32_t*)v.LTcol, (const double*)v.LTval, zn, z,
                (const int64_t*)v.Vptr, (const int32_t*)v.Vcol, (const double*)v.Vval, (const double*)v.rF);
+}
+
+// kernel choice of a level's two substitutions: lanes per row, staged variants, and on large
+// levels the row partition of the persistent ring kernels (AJ_APPLY_RING=0: off;
+// AJ_RING_MIN: smallest entry count that takes them)
+static void plan_apply(Level& v, cudaStream_t st) {
+  v.gf = pick_group(v.nC ? (double)v.nnzL / v.nC : 1.0, v.nnzL);
+  // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
+  v.gb = pick_group(v.nF ? (double)v.nnzLT / v.nF : 1.0, v.nnzLT, v.nF <= 2048 ? TB : 32);
+  if (const char* fg = getenv("AJ_FORCE_GB")) v.gb = atoi(fg);  // testing: every backward group size
+  v.nst_f = pick_stages(v.nnzL, v.nC, v.gf);
+  v.nst_b = pick_stages(v.nnzLT, v.nF, v.gb);
+  for (void* q : {(void*)v.fpart, (void*)v.bpart, (void*)v.yv, (void*)v.dF}) dfree(q, st);
+  v.fpart = v.bpart = nullptr;
+  v.yv = v.dF = nullptr;
+  v.nfpart = v.nbpart = 0;
+  const char* ring = getenv("AJ_APPLY_RING");
+  const char* rmin = getenv("AJ_RING_MIN");
+  const int64_t ring_min = rmin ? atoll(rmin) : (int64_t(1) << 22);
+  if (ring && atoi(ring) != 0 && v.nst_f == 0 && v.nC > 0 && v.nnzL >= ring_min) {
+    v.nfpart = (int)std::min<int64_t>(num_sms() * RING_CTAS, std::max<int64_t>(1, v.nnzL / (2 * RCAP)));
+    v.fpart = dalloc<int32_t>(v.nfpart + 1, st);
+    k_row_partition<<<ceil_div(v.nfpart + 1, TB), TB, 0, st>>>(v.nC, v.Lptr, v.nfpart, v.fpart);
+    AJ_LAUNCHED();
+    const char* rb = getenv("AJ_APPLY_RING_BWD");  // testing: 0 keeps the register backward kernels
+    if (!(rb && atoi(rb) == 0) && v.nst_b == 0 && v.nF > 0 && v.gb <= 32) {
+      v.nbpart = (int)std::min<int64_t>(num_sms() * RING_CTAS, std::max<int64_t>(1, v.nnzLT / (2 * RCAP)));
+      v.bpart = dalloc<int32_t>(v.nbpart + 1, st);
+      k_row_partition<<<ceil_div(v.nbpart + 1, TB), TB, 0, st>>>(v.nF, v.LTptr, v.nbpart, v.bpart);
+      AJ_LAUNCHED();
+      v.yv = dalloc<double>(v.nF, st);
+      v.dF = dalloc<double>(v.nF, st);
+    }
+  }
 }
 
 // forward step of level v: r -> rn (the next level's input), and, if `nxt` is a sparse
@@ -1516,9 +1969,18 @@ __global__ void k_dense_mv(int n, const double* __restrict__ G, const double* __
   pdl_wait();
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * TB + threadIdx.x) >> 5; i < n; i += (gridDim.x * TB) >> 5) {
-    double acc = 0.0;
-    for (int j = lane; j < n; j += 32) acc += G[(int64_t)i * n + j] * r[j];
-    acc = warp_sum(acc);
+    // four independent partial sums per lane: loads of four 256-byte row segments in flight
+    const double* __restrict__ Gi = G + (int64_t)i * n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = lane;
+    for (; j + 96 < n; j += 128) {
+      a0 += Gi[j] * r[j];
+      a1 += Gi[j + 32] * r[j + 32];
+      a2 += Gi[j + 64] * r[j + 64];
+      a3 += Gi[j + 96] * r[j + 96];
+    }
+    for (; j < n; j += 32) a0 += Gi[j] * r[j];
+    const double acc = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) z[i] = acc;
   }
 }
@@ -1597,7 +2059,7 @@ void Csr::release(cudaStream_t st) {
 void Level::release(cudaStream_t st) {
   for (void* p : {(void*)D, (void*)cmap, (void*)cidx, (void*)fidx, (void*)fmap, (void*)partner, (void*)b11, (void*)b12,
                   (void*)Lptr, (void*)Lcol, (void*)Lval, (void*)LTptr, (void*)LTcol, (void*)LTval, (void*)Vptr,
-                  (void*)Vcol, (void*)Vval, (void*)r, (void*)z, (void*)rF})
+                  (void*)Vcol, (void*)Vval, (void*)r, (void*)z, (void*)rF, (void*)fpart, (void*)bpart, (void*)yv, (void*)dF})
     dfree(p, st);
 }
 
@@ -1939,12 +2401,7 @@ Precond* precond_create_slab(const double* eps, int L, int z0, int nz, bool open
         lv.z = dalloc<double>(lv.n, st);
         lv.rF = dalloc<double>(std::max(lv.nF, 1), st);
       }
-      lv.gf = pick_group(lv.nC ? (double)lv.nnzL / lv.nC : 1.0, lv.nnzL);
-      // few long L^T rows (deep levels): up to a CTA per row; else at most a warp per row
-      lv.gb = pick_group(lv.nF ? (double)lv.nnzLT / lv.nF : 1.0, lv.nnzLT, lv.nF <= 2048 ? TB : 32);
-      if (const char* fg = getenv("AJ_FORCE_GB")) lv.gb = atoi(fg);    // testing: every backward group size
-      lv.nst_f = pick_stages(lv.nnzL, lv.nC, lv.gf);
-      lv.nst_b = pick_stages(lv.nnzLT, lv.nF, lv.gb);
+      plan_apply(lv, st);
       K->lv.push_back(lv);
       A.release(st);
       A = S;
@@ -2276,8 +2733,7 @@ static void inverse_based_drop(Precond* K, double tau, cudaStream_t st) {
     v.LTcol = LTcol2;
     v.LTval = LTval2;
     v.nnzL = v.nnzLT = nL2;
-    v.gf = pick_group(v.nC ? (double)v.nnzL / v.nC : 1.0, v.nnzL);
-    v.gb = pick_group(v.nF ? (double)v.nnzLT / v.nF : 1.0, v.nnzLT, v.nF <= 2048 ? TB : 32);
+    plan_apply(v, st);
   }
   dfree(ndrop, st);
   for (double* p : x) dfree(p, st);

@@ -45,6 +45,11 @@ struct Level {
   int64_t nnzV = 0;
   int gf = 1, gb = 1;           // threads per row of the forward / backward kernels
   int nst_f = 0, nst_b = 0;     // shared-memory stages of the staged kernels (0: register prefetch)
+  int32_t* fpart = nullptr;     // nfpart+1 row boundaries of the persistent ring forward kernel (large levels)
+  int32_t* bpart = nullptr;     // nbpart+1, backward
+  int nfpart = 0, nbpart = 0;
+  double* yv = nullptr;         // nF  backward right-hand side B~^{-1}(D r)_F, written by the ring forward kernel
+  double* dF = nullptr;         // nF  D on the pivots, compact
   double* rF = nullptr;         // nF: r on the pivots, compact (levels >= 1; written by the previous forward step)
   double* r = nullptr;          // level workspace (levels >= 1)
   double* z = nullptr;

@@ -338,8 +338,7 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
           for (int64_t ev = a.Vptr[u]; ev < a.Vptr[u + 1]; ++ev) {
             const int32_t v = a.Vcol[ev];
             const int q = atomicAdd(&s_nvt[grp], 1);
-            const uint32_t k0 = (uint32_t)min(u, v), k1 = (uint32_t)max(u, v);
-            sk[q] = ((uint64_t)k0 << 32) | k1;
+            sk[q] = ((uint64_t)(uint32_t)v << 32) | (uint32_t)u;  // (target x, source pivot u)
             sp[q] = q;
             VTx[q] = v;
             VTt[q] = __dmul_rn(acu, a.Vval[ev]);
@@ -365,7 +364,9 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     }
     gsync<G, GROUPS>();
     SPROF(0);
-    // ---- (A2) virtual terms in ascending block key, accumulated into l^v (serial)
+    // ---- (A2) virtual terms accumulated into l^v in ascending block key {u, x}: for a fixed
+    // target x that is ascending source pivot u, so the terms are sorted by (x, u) and one
+    // thread per target sums its run in order (the oracle's order, bitwise)
     const int nvt = s_nvt[grp];
     if (nvt > 0) {
       const int P = pow2_at_least(nvt);
@@ -375,22 +376,26 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       }
       gsync<G, GROUPS>();
       group_bitonic<G, GROUPS>(sk, sp, P, tid);
-      if (tid == 0) {
-        for (int i = 0; i < nvt; ++i) {
-          const int q = sp[i];
-          const int32_t x = VTx[q];
-          bool fr;
-          const int pos = lslot<T>(tab, vals, x, &s_cnt[grp], list, &fr);
-          if (fr) {
-            Lx[pos] = x;
-            Lr[pos] = 0.0;
-            Lv[pos] = 0.0;
-            Lfl[pos] = 2;
-          } else {
-            Lfl[pos] |= 2;
-          }
-          Lv[pos] = __dadd_rn(Lv[pos], VTt[q]);
+      for (int i = tid; i < nvt; i += G) {
+        const int q = sp[i];
+        const int32_t x = VTx[q];
+        if (i > 0 && VTx[sp[i - 1]] == x) continue;  // not the head of its run
+        double sum = VTt[q];
+        for (int j = i + 1; j < nvt; ++j) {
+          const int qj = sp[j];
+          if (VTx[qj] != x) break;
+          sum = __dadd_rn(sum, VTt[qj]);
         }
+        bool fr;
+        const int pos = lslot<T>(tab, vals, x, &s_cnt[grp], list, &fr);
+        if (fr) {
+          Lx[pos] = x;
+          Lr[pos] = 0.0;
+          Lfl[pos] = 2;
+        } else {
+          Lfl[pos] |= 2;
+        }
+        Lv[pos] = sum;
       }
       gsync<G, GROUPS>();
     }

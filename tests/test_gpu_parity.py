@@ -250,12 +250,15 @@ def oracle_l48(gpu_lib):
                                      {"AJ_SCHUR_TIER": "3"}, {"AJ_SCHUR_TIER": "4"}, {"AJ_SCHUR_TIER": "5"},
                                      {"AJ_FORCE_GB": "64"}, {"AJ_FORCE_GB": "256"}, {"AJ_GJ_STEPS": "1"},
                                      {"AJ_GJ_UNBLOCKED": "1"},
-                                     {"AJ_APPLY_STAGED": "1"}, {"AJ_APPLY_STAGED": "1", "AJ_FORCE_GB": "128"}])
+                                     {"AJ_APPLY_STAGED": "1"}, {"AJ_APPLY_STAGED": "1", "AJ_FORCE_GB": "128"},
+                                     {"AJ_APPLY_RING": "1", "AJ_RING_MIN": "1"},
+                                     {"AJ_APPLY_RING": "1", "AJ_RING_MIN": "100000", "AJ_APPLY_RING_BWD": "0"}])
 def test_precond_parity_production_l48(gpu_lib, monkeypatch, oracle_l48, variant):
     # GPU vs ORACLE at a size spanning many tiles (24 levels, coarse ~900) with the production
     # parameters, once with the routed default and once with each kernel variant forced
     # (row-group lanes, every Schur tier, CTA-per-row backward, the swap-based coarse inverse,
-    # the bulk-copy staged substitution kernels)
+    # the bulk-copy staged substitution kernels, the opt-in persistent ring kernels on every
+    # level / forward only on the larger levels)
     import torch
     o = oracle_l48
     for k, v in variant.items():

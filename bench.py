@@ -186,7 +186,7 @@ def _oracle_solve(job):
         e = an.disorder(L, W, seed)
         A = an.matrix(L, e, hop=hop)
         td, ts, tv = resolved_drop(L)    # the GPU path's default parameters (R12, R17)
-        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=1024,
+        M = mlildl.MultilevelILDL(an.matrix(L, e, hop=hop, sigma=sigma), lattice_L=L, n_coarse_max=2048,
                                   tau_drop=td, tau_strong=ts, tau_virtual=tv)
         lam, X, st = jd_nearest(A, M.apply, k, sigma=sigma, tol=tol)
         dt = time.perf_counter() - t0

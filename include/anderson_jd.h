@@ -108,7 +108,7 @@ typedef struct {
   int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
   int32_t max_levels;    /* level cap (<= 1023)                                  */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
-  int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN)      */
+  int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN); default 40960 */
   int32_t cand_cap;      /* reserved (>= 64)                                     */
   int32_t factor_fp32;   /* 1: store L / L^T values in fp32 (fp64 accumulation)  */
   int32_t compensate;    /* 1: first-order treatment of the dropped weak pivot-pivot

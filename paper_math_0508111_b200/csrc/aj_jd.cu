@@ -80,8 +80,14 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
   double* AV = dalloc<double>(n * jmax, st);
   double* Vt = dalloc<double>(n * jmax, st);
   double* AVt = dalloc<double>(n * jmax, st);
-  double* QT = dalloc<double>(n * (k + 2), st);
-  double* Y = dalloc<double>(n * (k + 2), st);
+  // missed-eigenvalue safeguard (R15): after the k-th pair is locked, a Ritz value of the
+  // remaining search space nearer to sigma than the farthest of the k locked pairs keeps JD going
+  // for up to `extra` more pairs; the k nearest of all locked pairs are returned
+  // (AJ_JD_EXTRA, testing: 0 = stop at the k-th pair as round 1 did)
+  const char* exenv = getenv("AJ_JD_EXTRA");
+  const int extra = std::max(0, std::min(exenv ? atoi(exenv) : 2, 17 - k));  // m = nq + 1 <= 17 (k_small_inv)
+  double* QT = dalloc<double>(n * (k + extra + 2), st);
+  double* Y = dalloc<double>(n * (k + extra + 2), st);
   double* u = dalloc<double>(n, st);
   double* Au = dalloc<double>(n, st);
   double* r = dalloc<double>(n, st);
@@ -191,9 +197,23 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
         if (jp.verbose)
           fprintf(stderr, "[jd] converged %d: lambda=%.15g |r|=%.3e outer=%d inner=%d\n", nq, sigma + theta0,
                   rnorm, R.outer, R.inner_total);
-        if (nq == k) {
-          done = true;
-          break;
+        if (nq >= k) {
+          bool more = false;
+          if (nq < k + extra && j >= 2) {
+            std::vector<double> dist;
+            for (double l : lam) dist.push_back(fabs(l - sigma));
+            std::nth_element(dist.begin(), dist.begin() + (k - 1), dist.end());
+            double th1;
+            rd(&th1, theta + 1, 1, st);  // the nearest Ritz value of the space without the locked vector
+            more = fabs(th1) < dist[k - 1];
+            if (more && jp.verbose)
+              fprintf(stderr, "[jd] %d pairs locked, but a Ritz value at distance %.6e < %.6e remains: continuing\n",
+                      nq, fabs(th1), dist[k - 1]);
+          }
+          if (!more) {
+            done = true;
+            break;
+          }
         }
         if (j == 1) {
           j = 0;
@@ -260,7 +280,22 @@ JdResult jd_run(int k, double sigma, double tol, const double* eps, const Domain
         fprintf(stderr, "[jd] outer %d j=%d theta=%.6e |r|=%.3e inner=%d relres=%.2e%s\n", R.outer, j, theta0,
                 rnorm, sr.iters, sr.relres, sr.breakdown ? " (breakdown)" : "");
     }
-    // results: eigenvalues, recomputed residuals, eigenvectors
+    // results: eigenvalues, recomputed residuals, eigenvectors -- of more than k locked pairs
+    // (safeguard above) the k nearest sigma, in the order they converged
+    if (nq > k) {
+      std::vector<int> idx(nq);
+      for (int i = 0; i < nq; ++i) idx[i] = i;
+      std::stable_sort(idx.begin(), idx.end(),
+                       [&](int a, int c) { return fabs(lam[a] - sigma) < fabs(lam[c] - sigma); });
+      idx.resize(k);
+      std::sort(idx.begin(), idx.end());
+      for (int i = 0; i < k; ++i) {
+        if (idx[i] != i) launch_copy(QT + (int64_t)i * n, QT + (int64_t)idx[i] * n, n, st);
+        lam[i] = lam[idx[i]];
+      }
+      lam.resize(k);
+      nq = k;
+    }
     R.converged = nq;
     for (int i = 0; i < nq; ++i) h_lambda[i] = lam[i];
     if (h_resid) {

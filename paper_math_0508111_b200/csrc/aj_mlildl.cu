@@ -1399,7 +1399,7 @@ __global__ void __launch_bounds__(TB, 6)
   }
 }
 
-// ---- persistent ring apply (DESIGN.md sect. 4) ------------------------------------------
+// ---- persistent ring apply (DESIGN.md sect. 4; opt-in, AJ_APPLY_RING=1) ------------------
 // Large levels: one CTA per SM owns a run of consecutive rows holding ~1/grid of the level's
 // factor entries (row partition `part`, balanced by entries at setup).  A producer warp streams
 // the CTA's contiguous (index, value) range through a ring of RNST shared-memory stages with 1-D
@@ -1408,21 +1408,24 @@ __global__ void __launch_bounds__(TB, 6)
 // entries, gathers the predecessor's output (PREF independent gathers per batch), reduces over
 // the G lanes of a row and writes.  Every warp passes every stage in order (wait full, then
 // arrive empty), so a stage is refilled only when all warps are past it.  The factor stream
-// never waits behind a row pointer or a gather; the first RNST stages are issued before
-// griddepcontrol.wait, and a CTA takes less than half an SM's shared memory and threads so the
-// next level's CTAs are resident (prefetching) while this level runs.  Row metadata is loaded
-// one tile ahead.
+// never waits behind a row pointer or a gather, and the first RNST stages are issued before
+// griddepcontrol.wait.  Row metadata is loaded one tile ahead.
+// Measured (profiles/round2_s5_apply_experiments.txt, L=150): 16 warps + 4 x 2048-entry stages
+// at one CTA per SM (so that the next level's CTAs are co-resident) 4.61 ms; 2 CTAs per SM with
+// 8 x 1024 3.76 ms; 28 warps + 16 x 1024 (192 KB, the defaults below) 3.63 ms -- against 3.67 ms
+// of the register-prefetch kernels: the consumers' gather latency, not the factor stream, is the
+// bound, so the ring buys nothing and stays opt-in.
 #ifndef AJ_RCAP
-#define AJ_RCAP 2048
-#define AJ_RNST 4
-#define AJ_RNW 16
+#define AJ_RCAP 1024
+#define AJ_RNST 16
+#define AJ_RNW 28
 #define AJ_RING_CTAS 1
 #endif
 #ifndef AJ_RING_MINB
-#define AJ_RING_MINB 2  // two resident CTAs per SM: this level's and the next level's (prefetching)
+#define AJ_RING_MINB 1
 #endif
-constexpr int RCAP = AJ_RCAP;  // entries per stage: 8 KB indices + 16 KB fp64 values
-constexpr int RNST = AJ_RNST;  // stages (96 KB)
+constexpr int RCAP = AJ_RCAP;  // entries per stage: 4 KB indices + 8 KB fp64 values
+constexpr int RNST = AJ_RNST;  // stages (192 KB)
 constexpr int RNW = AJ_RNW;    // consumer warps
 constexpr int RING_CTAS = AJ_RING_CTAS;  // ring CTAs per SM
 constexpr int RTB = RNW * 32 + 32;  // + the producer warp

@@ -23,6 +23,8 @@ binding.anderson_build(eps, L, cfg["W"], cfg["seed"])
 pp = binding.default_precond_params()
 if "AJ_TD" in os.environ:
     pp.tau_drop = float(os.environ["AJ_TD"])
+if "AJ_NCOARSE" in os.environ:
+    pp.n_coarse_max = int(os.environ["AJ_NCOARSE"])
 st = torch.cuda.current_stream()
 for i in range(reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,5 +34,6 @@ for i in range(reps):
     e1.record(st)
     e1.synchronize()
     print(json.dumps(dict(i=i, ms=e0.elapsed_time(e1), wall_ms=(time.perf_counter() - t0) * 1e3,
-                          setup_ms=s["setup_ms"], solve_ms=s["solve_ms"], outer=s["outer"], inner=s["inner_total"])),
+                          setup_ms=s["setup_ms"], solve_ms=s["solve_ms"], outer=s["outer"], inner=s["inner_total"],
+                          levels=s["precond"]["levels"], coarse=s["precond"]["coarse_n"])),
           flush=True)

@@ -596,6 +596,49 @@ def test_jd_config2_l100_properties(gpu_lib):
     assert np.allclose(np.sort(lam1), np.sort(lam2), atol=1e-10 * normA)
 
 
+def test_jd_config4_l250_properties(gpu_lib):
+    # BASELINE configs[4] at full size (n = 15,625,000, W = 16.5, seed 4) on one GPU, the
+    # north star's target lattice: residuals recomputed with the oracle stencil, Rayleigh
+    # quotients, orthonormality, interior eigenvalues (~1 min of GPU time)
+    cfg = CONFIGS[4]
+    L, W, seed, hop, k = cfg["L"], 16.5, 4, cfg["hop"], cfg["k"]
+    assert L == 250
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    e = an.disorder(L, W, seed)
+    normA = 6 + np.abs(e).max()
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop)
+    Xh = N(X)
+    for i in range(k):
+        ax = an.stencil_apply(L, e, Xh[:, i], hop=hop)
+        assert np.linalg.norm(ax - lam[i] * Xh[:, i]) <= 1e-8 * normA
+        assert abs(Xh[:, i] @ ax - lam[i]) <= 1e-10 * normA
+        assert res[i] <= 1e-8 * normA
+    assert np.abs(Xh.T @ Xh - np.eye(k)).max() <= 1e-8
+    assert np.abs(lam).max() < 1e-4   # interior: the level spacing near 0 at n = 1.6e7 is ~5e-7
+
+
+def test_jd_config4_w12_l100_properties(gpu_lib):
+    # BASELINE configs[4]'s hardest disorder, W = 12 (seed 4), at L = 100 (Table 4,
+    # l.1235-1237: JD + ILUPACK at W=12 up to M=130): the independent-set levels densify and
+    # stall on a coarse block of ~12.7k unknowns, inverted densely (blocked Gauss-Jordan) under
+    # the default dense_cap.  Size-independent properties against the oracle stencil.
+    cfg = CONFIGS[4]
+    L, W, seed, hop, k = 100, 12.0, 4, cfg["hop"], cfg["k"]
+    eps = gpu_eps(gpu_lib, L, W, seed)
+    e = an.disorder(L, W, seed)
+    normA = 6 + np.abs(e).max()
+    lam, X, res, st = gpu_lib.jd_solve(k, 0.0, cfg["tol"], eps, L, hop)
+    assert st["precond"]["coarse_n"] > 4096   # the stalled, densely inverted coarse block
+    Xh = N(X)
+    for i in range(k):
+        ax = an.stencil_apply(L, e, Xh[:, i], hop=hop)
+        assert np.linalg.norm(ax - lam[i] * Xh[:, i]) <= 1e-8 * normA
+        assert abs(Xh[:, i] @ ax - lam[i]) <= 1e-10 * normA
+        assert res[i] <= 1e-8 * normA
+    assert np.abs(Xh.T @ Xh - np.eye(k)).max() <= 1e-8
+    assert np.abs(lam).max() < 1e-3
+
+
 def test_jd_config3_l200_properties(gpu_lib):
     # BASELINE configs[3] at full size (n = 8*10^6) on one GPU: residuals recomputed with
     # the oracle stencil (north-star bounds: ||Ax - lambda x|| <= 1e-8 ||A||), Rayleigh

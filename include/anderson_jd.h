@@ -105,7 +105,7 @@ typedef struct {
   double tau_strong;     /* strong-coupling threshold of the independent sets;
                             < 0: auto, min(0.05, 40 tau_drop) with compensation,
                             else 10 * tau_drop                                    */
-  int32_t n_coarse_max;  /* stop recursing at this size, invert densely          */
+  int32_t n_coarse_max;  /* stop recursing at this size, invert densely; default 2048 */
   int32_t max_levels;    /* level cap (<= 1023)                                  */
   double stall_frac;     /* stop when a level eliminates < stall_frac * n        */
   int32_t dense_cap;     /* largest coarse system accepted (else BREAKDOWN); default 40960 */

@@ -256,6 +256,25 @@ __device__ void group_bitonic(K* k, V* v, int P, int tid) {
     }
 }
 
+// rank sort of n <= RANK_MAX distinct keys in group scratch: every element counts the keys below
+// it (n independent broadcast loads instead of the log^2 n dependent exchange stages of the
+// bitonic network, each a round trip to the scratch in L2) and writes its index to v[rank].
+// Same result as group_bitonic on (k, identity): v = the permutation that sorts k; k is left as is.
+constexpr int RANK_MAX = 128;
+template <int G, int GROUPS, typename K, typename V>
+__device__ void group_ranksort(const K* k, V* v, int n, int tid) {
+  for (int i = tid; i < n; i += G) {
+    const K ki = k[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const K kj = k[j];
+      r += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
+    }
+    v[r] = (V)i;
+  }
+  gsync<G, GROUPS>();
+}
+
 __host__ __device__ constexpr int pow2_at_least(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -369,13 +388,18 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     // thread per target sums its run in order (the oracle's order, bitwise)
     const int nvt = s_nvt[grp];
     if (nvt > 0) {
-      const int P = pow2_at_least(nvt);
-      for (int t = nvt + tid; t < P; t += G) {
-        sk[t] = ~0ull;
-        sp[t] = t;
+      if (nvt <= RANK_MAX) {
+        gsync<G, GROUPS>();
+        group_ranksort<G, GROUPS>(sk, sp, nvt, tid);
+      } else {
+        const int P = pow2_at_least(nvt);
+        for (int t = nvt + tid; t < P; t += G) {
+          sk[t] = ~0ull;
+          sp[t] = t;
+        }
+        gsync<G, GROUPS>();
+        group_bitonic<G, GROUPS>(sk, sp, P, tid);
       }
-      gsync<G, GROUPS>();
-      group_bitonic<G, GROUPS>(sk, sp, P, tid);
       for (int i = tid; i < nvt; i += G) {
         const int q = sp[i];
         const int32_t x = VTx[q];
@@ -407,14 +431,17 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
       sk[pos] = (uint64_t)(uint32_t)Lx[pos];
       sp[pos] = pos;
     }
-    {
+    if (nl <= RANK_MAX) {
+      gsync<G, GROUPS>();
+      if (nl > 1) group_ranksort<G, GROUPS>(sk, sp, nl, tid);
+    } else {
       const int P = pow2_at_least(nl);
       for (int t = nl + tid; t < P; t += G) {
         sk[t] = ~0ull;
         sp[t] = t;
       }
       gsync<G, GROUPS>();
-      if (nl > 1) group_bitonic<G, GROUPS>(sk, sp, P, tid);
+      group_bitonic<G, GROUPS>(sk, sp, P, tid);
     }
     SPROF(2);
     for (int i = tid; i < nl; i += G) {
@@ -458,15 +485,23 @@ __global__ void __launch_bounds__(G * GROUPS, 1)  // minBlocks 1: no register ca
     SPROF(4);
     // ---- (C) real terms, x ascending; (D) virtual terms on the pattern, x ascending
     // work lists of (C) and (D): the sorted L-row positions with real / virtual terms
-    if (tid == 0) {
+    if (tid < 32) {  // the group's first warp: stable compaction, 32 positions per ballot
       int nr = 0, nv2 = 0;
-      for (int i = 0; i < nl; ++i) {
-        const int fl = Xf[i];
-        if (fl & 1) sp[nr++] = i;
-        if (fl & 2) VTx[nv2++] = i;
+      const unsigned lower = (1u << tid) - 1u;
+      for (int i0 = 0; i0 < nl; i0 += 32) {
+        const int i = i0 + tid;
+        const int fl = (i < nl) ? Xf[i] : 0;
+        const unsigned br = __ballot_sync(0xffffffffu, (fl & 1) != 0);
+        const unsigned bv = __ballot_sync(0xffffffffu, (fl & 2) != 0);
+        if (fl & 1) sp[nr + __popc(br & lower)] = i;
+        if (fl & 2) VTx[nv2 + __popc(bv & lower)] = i;
+        nr += __popc(br);
+        nv2 += __popc(bv);
       }
-      s_nvt[grp] = nr;   // reused: number of real items
-      s_kept[grp] = nv2; // reused: number of virtual items (s_kept is reset below)
+      if (tid == 0) {
+        s_nvt[grp] = nr;   // reused: number of real items
+        s_kept[grp] = nv2; // reused: number of virtual items (s_kept is reset below)
+      }
     }
     gsync<G, GROUPS>();
     const int nitems[2] = {s_nvt[grp], s_kept[grp]};

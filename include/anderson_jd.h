@@ -195,7 +195,13 @@ AJ_API int ortho_cgs2(double* d_x, const double* d_V, int32_t m, int64_t n, doub
  * multilevel ILDL at sigma; thick restart; deflation of converged pairs.
  * Converged when ||A x - lambda x||_2 <= tol * ||A||_1, ||A||_1 = 6|hop| + max|eps|.
  *
- * d_eps: device n doubles.  h_lambda: host k (out, sorted by |lambda - sigma|).
+ * JD locks the Ritz pair nearest sigma as it converges, which is usually, not
+ * provably, the order of distance from sigma; after the k-th pair a Ritz value
+ * of the remaining search space nearer to sigma than the farthest locked pair
+ * keeps the iteration going for up to 2 more pairs, and the k nearest of all
+ * locked pairs are returned (R15; a heuristic, not a certificate).
+ *
+ * d_eps: device n doubles.  h_lambda: host k (out, in the order the pairs converged).
  * d_X: device n*k (out, orthonormal eigenvectors, may be NULL).
  * h_resid: host k (out, ||A x - lambda x||_2 recomputed after convergence).
  * Returns AJ_ERR_NOCONV (with the converged prefix filled) if max_outer is hit.
